@@ -1,0 +1,232 @@
+"""Pins the C oracle (oracle/mla_oracle.c) bit-for-bit to outputs of the unmodified reference
+(tests/golden/golden_small.npz, produced by tests/golden/make_golden.py) and to the reference's own
+known-answer tests (pkg/tests/test_lu.py, test_kernels.py, test_oracle.py -- cited per test)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import cases
+import oracle
+from paper_1611_06365_b200.workloads import make_matrix, splitmix64_uniform01
+
+
+def gen(m, n, seed):
+    return cases.uniform_pm1(oracle.fill_random, m, n, seed)
+
+
+def same(a, b):
+    return a.shape == b.shape and np.array_equal(np.asarray(a), np.asarray(b))
+
+
+def test_fill_random_bitwise(golden):
+    a = oracle.alloc(7, 5, ld=9)
+    oracle.fill_random(a, 3)
+    assert same(a, golden["fill_7x5_seed3"])
+    # host numpy twin used by the workload generators
+    assert same(splitmix64_uniform01(7, 5, 3), golden["fill_7x5_seed3"])
+    # counter-based: a column block is independently computable
+    assert same(splitmix64_uniform01(7, 5, 3, col0=2, ncols=2), golden["fill_7x5_seed3"][:, 2:4])
+
+
+@pytest.mark.parametrize("c", cases.UNB, ids=lambda c: c["name"])
+def test_unb_bitwise(golden, c):
+    a = gen(c["m"], c["n"], c["seed"])
+    r = oracle.unb_pivoted(a)
+    assert same(r.ipiv, golden[c["name"] + "/ipiv"])
+    assert same(a, golden[c["name"] + "/lu"])
+
+
+@pytest.mark.parametrize("c", cases.LL, ids=lambda c: c["name"])
+def test_blk_ll_bitwise(golden, c):
+    a = gen(c["m"], c["n"], c["seed"])
+    r = oracle.lu_blk_ll(a, c["b"], stop_trip=c["stop_trip"], k_c=c["k_c"])
+    assert r.cols_factored == int(golden[c["name"] + "/cols"][0])
+    assert same(r.ipiv, golden[c["name"] + "/ipiv"])
+    assert same(a, golden[c["name"] + "/lu"])
+
+
+@pytest.mark.parametrize("c", cases.RL, ids=lambda c: c["name"])
+def test_blk_rl_bitwise(golden, c):
+    a = gen(c["m"], c["n"], c["seed"])
+    r = oracle.lu_blk_rl(a, c["b"], inner_b=c["inner_b"])
+    assert same(r.ipiv, golden[c["name"] + "/ipiv"])
+    assert same(a, golden[c["name"] + "/lu"])
+
+
+@pytest.mark.parametrize("c", cases.LA, ids=lambda c: c["name"])
+def test_lu_la_bitwise(golden, c):
+    a = gen(c["m"], c["n"], c["seed"])
+    r = oracle.lu_la(a, c["b_o"], c["b_i"], k_c=c["k_c"])
+    assert same(r.ipiv, golden[c["name"] + "/ipiv"])
+    assert same(a, golden[c["name"] + "/lu"])
+    assert r.et_events == 0
+
+
+@pytest.mark.parametrize("c", cases.LA_ET, ids=lambda c: c["name"])
+def test_lu_la_et_replay_bitwise(golden, c):
+    a = gen(c["m"], c["n"], c["seed"])
+    r = oracle.lu_la(a, c["b_o"], c["b_i"], et_sched=c["sched"], k_c=c["k_c"])
+    assert r.et_events == int(golden[c["name"] + "/et_events"][0])
+    cut = [w for w, full in zip(r.widths[1:], _full_widths(r.widths, c)) if w < full]
+    assert cut == list(golden[c["name"] + "/et_widths"])
+    assert same(r.ipiv, golden[c["name"] + "/ipiv"])
+    assert same(a, golden[c["name"] + "/lu"])
+    assert all(w > 0 and (w % c["b_i"] == 0) for w in cut)  # test_lu.py:215-223
+
+
+def _full_widths(widths, c):
+    """Scheduled width of every iteration after the prologue, replaying lu.py:318-323."""
+    out, b_target, q1 = [], c["b_o"], widths[0]
+    for k_new in widths[1:]:
+        w = min(b_target, c["n"] - q1)
+        out.append(w)
+        b_target = max(c["b_i"], k_new) if k_new < w else min(c["b_o"], 2 * b_target)
+        q1 += k_new
+    return out
+
+
+@pytest.mark.parametrize("c", cases.GEMM, ids=lambda c: c["name"])
+def test_gemm_bitwise(golden, c):
+    a = gen(c["m"], c["k"], c["seed"])
+    b = gen(c["k"], c["n"], c["seed"] + 100)
+    cc = gen(c["m"], c["n"], c["seed"] + 200)
+    oracle.gemm(cc, a, b, c["alpha"], c["beta"], k_c=c["k_c"])
+    assert same(cc, golden[c["name"] + "/c"])
+
+
+@pytest.mark.parametrize("c", cases.TRSM, ids=lambda c: c["name"])
+def test_trsm_bitwise(golden, c):
+    low = gen(c["w"], c["w"], c["seed"])
+    x = gen(c["w"], c["c"], c["seed"] + 100)
+    oracle.trsm_llu(low, x)
+    assert same(x, golden[c["name"] + "/x"])
+
+
+@pytest.mark.parametrize("c", cases.LASWP, ids=lambda c: c["name"])
+def test_laswp_bitwise(golden, c):
+    a = gen(c["rows"], c["cols"], c["seed"])
+    a0 = a.copy()
+    oracle.laswp(a, c["ipiv"])
+    assert same(a, golden[c["name"] + "/fwd"])
+    oracle.laswp(a, c["ipiv"], reverse=True)
+    assert same(a, golden[c["name"] + "/back"]) and same(a, a0)
+
+
+@pytest.mark.parametrize("c", cases.BIG, ids=lambda c: c["name"])
+def test_config_shaped_bitwise(golden, c):
+    a = np.asfortranarray(make_matrix(c["dist"], c["n"], c["seed"]))
+    a0 = a.copy(order="F")
+    r = oracle.lu_la(a, c["b_o"], c["b_i"])
+    assert np.array_equal(r.ipiv.astype(np.int32), golden[c["name"] + "/ipiv"])
+    digest = hashlib.sha256(a.tobytes(order="F")).digest()
+    assert digest == golden[c["name"] + "/sha"].tobytes()
+    # backward error bound of the reference's acceptance grid (test_acceptance.py:78-104)
+    n = c["n"]
+    assert oracle.residual_lu(a0, a, r.ipiv) <= n * 100 * np.finfo(np.float64).eps
+
+
+# ---- the reference's own known-answer tests, restated on the oracle --------------------------
+
+def test_kat_1x1_and_permutation():  # test_lu.py:29-42
+    a = np.array([[3.0]], order="F")
+    r = oracle.unb_pivoted(a)
+    assert list(r.ipiv) == [0] and a[0, 0] == 3.0
+    a = np.asfortranarray(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    r = oracle.unb_pivoted(a)
+    assert list(r.ipiv) == [1, 1] and not r.singular
+    assert np.array_equal(a, np.array([[1.0, 0.0], [0.0, 1.0]]))
+
+
+def test_kat_zero_pivot_column():  # test_lu.py:45-52
+    a = np.asfortranarray(np.array([[0.0, 2.0], [0.0, 3.0]]))
+    r = oracle.unb_pivoted(a)
+    assert r.singular and list(r.ipiv) == [0, 1]
+    assert np.array_equal(a[:, 0], [0.0, 0.0])
+
+
+def test_kat_wide_rejected():  # test_lu.py:55-57
+    with pytest.raises(ValueError):
+        oracle.unb_pivoted(oracle.alloc(2, 3))
+
+
+def test_kat_single_block_equals_unblocked():  # test_lu.py:74-82
+    a = gen(40, 24, 5)
+    b1, b2 = a.copy(order="F"), a.copy(order="F")
+    r0 = oracle.unb_pivoted(a)
+    r1 = oracle.lu_blk_ll(b1, 24)
+    r2 = oracle.lu_blk_rl(b2, 24)
+    assert same(a, b1) and same(a, b2)
+    assert same(r0.ipiv, r1.ipiv) and same(r0.ipiv, r2.ipiv)
+
+
+def test_kat_dominant_identity_pivots():  # test_lu.py:94-106
+    n = 300
+    rng = np.random.default_rng(0)
+    a = np.asfortranarray(rng.integers(-3, 4, size=(n, n)).astype(np.float64))
+    a[np.arange(n), np.arange(n)] = 4.0 * n
+    for b_o in (256, 128):
+        x = a.copy(order="F")
+        r = oracle.lu_la(x, b_o, 32)
+        assert np.array_equal(r.ipiv, np.arange(n))
+
+
+def test_kat_rl_ll_same_pivots():  # test_lu.py:121-129
+    a = gen(200, 96, 9)
+    x, y = a.copy(order="F"), a.copy(order="F")
+    assert same(oracle.lu_blk_rl(x, 32).ipiv, oracle.lu_blk_ll(y, 32).ipiv)
+
+
+def test_kat_et_cut_semantics():  # test_lu.py:132-170
+    a = gen(128, 128, 3)
+    ref = a.copy(order="F")
+    r = oracle.lu_blk_ll(a, 32, stop_trip=1)
+    assert r.cols_factored == 32
+    # the right columns carry exactly the first block's swaps and nothing else
+    oracle.laswp(ref[:, 32:], r.ipiv)
+    assert same(a[:, 32:], ref[:, 32:])
+    a = gen(128, 128, 3)
+    assert oracle.lu_blk_ll(a, 32, stop_trip=3).cols_factored == 96
+    a = gen(64, 32, 3)
+    assert oracle.lu_blk_ll(a, 32, stop_trip=1).cols_factored == 32  # single block never cut
+
+
+def test_kat_trsm_2x2_and_integer():  # test_kernels.py:279-283, test_oracle.py:29-36
+    low = np.asfortranarray(np.array([[9.0, 0.0], [2.0, 9.0]]))
+    x = np.asfortranarray(np.array([[1.0], [5.0]]))
+    oracle.trsm_llu(low, x)
+    assert np.array_equal(x, [[1.0], [3.0]])
+    low = np.asfortranarray(np.tril(np.arange(1.0, 17.0).reshape(4, 4)))
+    xs = np.asfortranarray(np.arange(1.0, 9.0).reshape(4, 2))
+    b = (np.tril(low, -1) + np.eye(4)) @ xs
+    b = np.asfortranarray(b)
+    oracle.trsm_llu(low, b)
+    assert np.array_equal(b, xs)
+
+
+def test_kat_laswp_single_swap_and_validation():  # test_kernels.py:329-332, 346-352
+    a = np.asfortranarray(np.arange(12.0).reshape(4, 3))
+    oracle.laswp(a, [2])
+    assert np.array_equal(a[0], [6.0, 7.0, 8.0]) and np.array_equal(a[2], [0.0, 1.0, 2.0])
+    before = a.copy()
+    with pytest.raises(IndexError):
+        oracle.laswp(a, [1, 4])
+    assert same(a, before)
+
+
+def test_kat_empty_and_singular_propagates():  # test_lu.py:234-244
+    r = oracle.lu_la(oracle.alloc(0, 0), 8, 4)
+    assert r.ipiv.size == 0 and not r.singular
+    a = gen(40, 40, 2)
+    a[:, 5] = 0.0
+    assert oracle.lu_la(a, 16, 4).singular
+
+
+def test_residual_grid():  # test_acceptance.py:78-104 (reduced grid)
+    eps = np.finfo(np.float64).eps
+    for n in (100, 500):
+        for b_o, b_i in ((32, 16), (128, 32), (256, 32)):
+            a = gen(n, n, 1)
+            a0 = a.copy(order="F")
+            r = oracle.lu_la(a, b_o, b_i)
+            assert oracle.residual_lu(a0, a, r.ipiv) <= n * 100 * eps
