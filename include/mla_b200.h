@@ -1,0 +1,136 @@
+/*
+ * mla_b200.h -- C ABI of the B200-native LU hot path (libmla_b200.so).
+ *
+ * The reference package `mla` (arXiv 1611.06365) is pure Python + numba and has no FFI of its own;
+ * its drop-in boundary is the module API in pkg/src/mla/__init__.py:6-33.  Each entry point below
+ * backs exactly one of those Python callables (cited per function); the ctypes binding a maintainer
+ * of the reference would add is shown in INTEGRATION.md and shipped as
+ * paper_1611_06365_b200/_capi.py.
+ *
+ * Conventions
+ *  - All matrices are column-major float64 in DEVICE memory unless the name ends in _host:
+ *    element (i,j) of a view is a[i + j*ld].  Views (sub-matrices) are expressed by pointer + ld,
+ *    exactly like the reference's numpy views (matrix.py:1-6).
+ *  - Pivots are int32 on the device (BASELINE.json), view-local, 0-based, ipiv[k] >= k
+ *    (matrix.py:74-92).  The Python layer widens to int64 (lu.py:86-89).
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*) unless stated.
+ *  - Return value: 0 on success, <0 on failure (MLA_E_*).  Nothing throws.  A numerically singular
+ *    matrix is NOT an error: it is reported through *singular (lu.py:56-59).
+ *  - The caller owns all matrices; the library owns only the workspace behind mla_handle.
+ *  - One handle per device, used from one host thread at a time (the reference's "collective over
+ *    a team" calling convention, pool.py:3-8, collapses to a single stream-ordered call).
+ */
+#ifndef MLA_B200_H
+#define MLA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mla_handle_s* mla_handle;
+
+enum {
+  MLA_OK = 0,
+  MLA_E_INVALID = -1,   /* shape / argument error -> ValueError in the Python layer          */
+  MLA_E_CUDA = -2,      /* a CUDA runtime call failed (mla_last_cuda_error gives the code)    */
+  MLA_E_ABORT = -3,     /* device-side watchdog fired (protocol bug / hang avoided)           */
+  MLA_E_INDEX = -4,     /* pivot index out of range -> IndexError (kernels.py:326-327)        */
+  MLA_E_NOMEM = -5
+};
+
+/* Scheduling variants of lu_la (config.py:12 VARIANTS). */
+enum {
+  MLA_VARIANT_LU = 0,        /* no look-ahead: update then panel, whole GPU as one team        */
+  MLA_VARIANT_LU_LA = 1,     /* look-ahead: panel team (sm_pf SMs) || update team              */
+  MLA_VARIANT_LU_WS_STATIC = 2, /* look-ahead + join at q column-chunk boundaries              */
+  MLA_VARIANT_LU_MB = 3,     /* look-ahead + worker sharing (panel SMs join the tile queue)    */
+  MLA_VARIANT_LU_ET = 4      /* + early termination of the panel by the update team            */
+};
+
+/* Outcome of a factorization -- mirrors LuResult (lu.py:33-41) plus the full width schedule. */
+typedef struct {
+  int32_t cols_factored;
+  int32_t singular;
+  int32_t et_events;
+  int32_t n_panels;         /* number of panels factored (prologue included)                  */
+  int32_t ws_joins;         /* iterations in which panel SMs joined the update queue (WS)     */
+  int32_t reserved[3];
+} mla_lu_info;
+
+/* Workspace / lifetime.  mla_create binds to `device` (cudaSetDevice) and sizes the persistent
+ * grid to the device's SM count.  Synchronous. */
+int mla_create(int device, mla_handle* out);
+int mla_destroy(mla_handle h);
+int mla_num_sms(mla_handle h);
+int mla_last_cuda_error(mla_handle h);
+const char* mla_version(void);
+
+/* gemm_malleable(c, a, b, alpha, beta, flag=...)  -- kernels.py:205-234.
+ * C (m x n) := alpha*C + beta*A(m x k)*B(k x n) on FP64 tensor cores.  m==0||n==0: no-op;
+ * k==0: C *= alpha.  join_flag (device word, nullable) is the WS entry point of the reference:
+ * `donor_ctas` CTAs of the grid stay out of the tile queue until *join_flag != 0 (polled at tile
+ * granularity), then join it; with a null flag every CTA works from the start. */
+int mla_gemm(mla_handle h, double* C, int64_t m, int64_t n, int64_t ldc, const double* A, int64_t lda,
+             const double* B, int64_t ldb, int64_t k, double alpha, double beta,
+             const uint32_t* join_flag, int donor_ctas, void* stream);
+
+/* trsm_llu(a11, b) -- kernels.py:264-293.  B (w x c) := trilu(L)^-1 B, unit diagonal never read. */
+int mla_trsm_llu(mla_handle h, const double* L, int64_t w, int64_t ldl, double* B, int64_t c,
+                 int64_t ldb, void* stream);
+
+/* laswp(a, piv, reverse) -- kernels.py:296-332.  Interchange t <-> ipiv[t] on every column of the
+ * rows x cols view, ascending (descending when reverse).  ipiv is a DEVICE int32 array; range
+ * validation happens on the device before anything is touched: on a bad index nothing is modified
+ * and the (synchronous) return value is MLA_E_INDEX. */
+int mla_laswp(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
+              int64_t npiv, int reverse, void* stream);
+
+/* lu_blk_ll(a, b, ipiv, stop) -- lu.py:140-180 (panel factorization, left-looking, inner block
+ * b_inner; b_inner >= w gives lu_unb, lu.py:97-103).  stop_flag (device word, nullable) is the ET
+ * flag: polled once per completed inner block while columns remain; stop_after_polls > 0 instead
+ * emulates the reference's CountingFlag fake (set from that poll on; test_lu.py:149-156).
+ * team_ctas <= 0 picks a team size from m.  Synchronous (returns the info). */
+int mla_panel_ll(mla_handle h, double* P, int64_t m, int64_t w, int64_t ld, int32_t* ipiv, int b_inner,
+                 const uint32_t* stop_flag, int stop_after_polls, int team_ctas, mla_lu_info* info,
+                 void* stream);
+
+/* lu_la(a, policy, pool) -- lu.py:197-334.  Whole factorization P*A = L*U in place, one persistent
+ * cooperative kernel: SM partition (sm_pf panel CTAs), atomic tile queue, WS and ET by device
+ * flags.  ipiv: device int32[n], global 0-based.  widths (device int32[widths_cap], nullable)
+ * receives every panel's factored width in order.  info_dev (device, nullable) receives the
+ * mla_lu_info; the call is asynchronous. */
+int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
+                 int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
+                 int32_t* widths, int widths_cap, void* stream);
+
+/* Same, reading the info back (synchronises the stream). */
+int mla_getrf_la_sync(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv,
+                      int b_outer, int b_inner, int variant, int sm_pf, int q_chunks,
+                      mla_lu_info* info_host, int32_t* widths_host, int widths_cap, void* stream);
+
+/* End-to-end form with HOST buffers (what bench.py's `e2e` times): uploads A (m x n, ld_host),
+ * factors on the device, downloads the packed factors and the pivots.  Synchronous. */
+int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_t ld_host,
+                      int32_t* ipiv_host, int b_outer, int b_inner, int variant, int sm_pf,
+                      int q_chunks, mla_lu_info* info_host);
+
+/* fill_random(a, seed) -- matrix.py:44-63: SplitMix64 stream, bit-identical to the reference;
+ * value = scale*u + shift with u in (0,1) (scale=1, shift=0 reproduces fill_random; 2,-1 gives the
+ * uniform[-1,1] configs).  col0/total_rows select a column block of a larger matrix (multi-GPU).
+ * row_scale (device, nullable): value *= row_scale[i]. */
+int mla_fill_random(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+                    int64_t col0, int64_t total_rows, double scale, double shift,
+                    const double* row_scale, void* stream);
+
+/* residual_lu(a_orig, L, U, piv) -- matrix.py:116-131: ||P*A - L*U||_F / ||A||_F from the packed
+ * factors, computed on the device (A_orig is destroyed: it is overwritten by P*A - L*U).
+ * Synchronous; result in *residual. */
+int mla_residual_lu(mla_handle h, double* A_orig, const double* LU, int64_t m, int64_t n, int64_t ld_a,
+                    int64_t ld_lu, const int32_t* ipiv, double* residual, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MLA_B200_H */

@@ -1,0 +1,222 @@
+// FP64 tensor-core (DMMA.8x8x4) tile multiply:  Cout = alpha*Cin + beta*(A @ B)  on one BM x BN
+// tile, all operands column-major.  This is the GPU replacement of the reference's packed
+// five-loop GEMM (kernels.py:42-160: _pack_a_slabs/_pack_b_slabs/_tile_product/_macro_block):
+//   * packing into slab buffers  -> cp.async (LDGSTS, 16 B, zero-fill at the fringes) into a
+//     STAGES-deep shared-memory ring; padding of 4 doubles per row makes every DMMA fragment
+//     load (LDS.64) bank-conflict free,
+//   * the m_r x n_r register micro-tile -> per-warp (WTI x WTJ) accumulator block of DMMA tiles,
+//   * ascending-k accumulation from zero, one owner per C element (kernels.py:3-9): kept, so the
+//     result does not depend on which CTA picked the tile or when.
+//
+// Orientation.  mma.m8n8k4 computes D(8x8) = A'(8x4,row) * B'(4x8,col).  We feed A' = U12^T-free:
+//   A'[r][k] = B[k][j0+r]   (the k x n operand, k contiguous in memory)
+//   B'[k][c] = A[i0+c][k]   (the m x k operand, i contiguous in memory)
+// so D[r][c] = sum_k A[i0+c][k] * B[k][j0+r] = (A@B)[i0+c][j0+r]: lane T ends up owning two
+// vertically adjacent C entries (rows i0+2*(T%4)+{0,1} of column j0+T/4), i.e. one aligned 16-byte
+// word of the column-major C.
+#pragma once
+#include "mla_common.cuh"
+
+namespace mla {
+
+template <int BM_, int BN_, int WI_, int WJ_, int STAGES_, int BK_ = 16>
+struct GemmCfg {
+  static constexpr int BM = BM_, BN = BN_, WI = WI_, WJ = WJ_, STAGES = STAGES_;
+  static constexpr int BK = BK_;
+  static constexpr int LDA_S = BM + 4;  // (BM+4) % 16 == 4 -> conflict-free fragment loads
+  static constexpr int LDB_S = BK + 4;
+  static constexpr int A_STAGE = BK * LDA_S;
+  static constexpr int B_STAGE = BN * LDB_S;
+  static constexpr int STAGE = A_STAGE + B_STAGE;  // doubles per stage
+  static constexpr int SMEM_BYTES = STAGES * STAGE * 8;
+  static constexpr int WTI = BM / WI, WTJ = BN / WJ;
+  static constexpr int NI = WTI / 8, NJ = WTJ / 8;
+  static_assert(WI * WJ * 32 == kThreads, "8 warps");
+  static_assert(BM % 16 == 0 && BN % 8 == 0 && WTI % 8 == 0 && WTJ % 8 == 0, "tile shape");
+};
+
+using GemmUpdateCfg = GemmCfg<128, 128, 2, 4, 3, 32>;  // trailing update tiles
+using GemmPanelCfg = GemmCfg<128, 32, 8, 1, 4>;    // panel-internal update (N = inner block)
+using GemmTrsmCfg = GemmCfg<32, 128, 1, 8, 4>;     // row-block update inside trsm strips
+
+// Issue the cp.async loads of k-tile `kt` into ring slot `slot`.
+template <class Cfg, bool AL16>
+__device__ __forceinline__ void gemm_load_stage(double* smem, int slot, const double* __restrict__ A,
+                                                int64_t lda, const double* __restrict__ B, int64_t ldb,
+                                                int K, int kt, int mrem, int nrem) {
+  double* sA = smem + slot * Cfg::STAGE;
+  double* sB = sA + Cfg::A_STAGE;
+  const int k0 = kt * Cfg::BK;
+  const int tid = threadIdx.x;
+  if (AL16) {
+    constexpr int ACH = Cfg::BM / 2;
+    for (int c = tid; c < Cfg::BK * ACH; c += kThreads) {
+      int kk = c / ACH, i = 2 * (c % ACH);
+      int valid = (k0 + kk < K) ? imin(imax(mrem - i, 0), 2) * 8 : 0;
+      const double* src = valid ? (A + (int64_t)(k0 + kk) * lda + i) : A;
+      cp_async16(sA + kk * Cfg::LDA_S + i, src, valid);
+    }
+    constexpr int BCH = Cfg::BK / 2;
+    for (int c = tid; c < Cfg::BN * BCH; c += kThreads) {
+      int j = c / BCH, kk = 2 * (c % BCH);
+      int valid = (j < nrem) ? imin(imax(K - (k0 + kk), 0), 2) * 8 : 0;
+      const double* src = valid ? (B + (int64_t)j * ldb + k0 + kk) : B;
+      cp_async16(sB + j * Cfg::LDB_S + kk, src, valid);
+    }
+  } else {
+    for (int c = tid; c < Cfg::BK * Cfg::BM; c += kThreads) {
+      int kk = c / Cfg::BM, i = c % Cfg::BM;
+      int valid = (k0 + kk < K && i < mrem) ? 8 : 0;
+      const double* src = valid ? (A + (int64_t)(k0 + kk) * lda + i) : A;
+      cp_async8(sA + kk * Cfg::LDA_S + i, src, valid);
+    }
+    for (int c = tid; c < Cfg::BN * Cfg::BK; c += kThreads) {
+      int j = c / Cfg::BK, kk = c % Cfg::BK;
+      int valid = (j < nrem && k0 + kk < K) ? 8 : 0;
+      const double* src = valid ? (B + (int64_t)j * ldb + k0 + kk) : B;
+      cp_async8(sB + j * Cfg::LDB_S + kk, src, valid);
+    }
+  }
+}
+
+// One C tile.  A: mrem x K (lda), B: K x nrem (ldb), Cin/Cout: mrem x nrem.  Cout may be shared
+// memory (generic pointer).  Collective over the CTA (256 threads); smem needs Cfg::SMEM_BYTES.
+template <class Cfg>
+__device__ void gemm_tile(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                          int64_t ldb, int K, const double* Cin, int64_t ldcin, double* Cout,
+                          int64_t ldcout, int mrem, int nrem, double alpha, double beta,
+                          double* smem) {
+  constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES, NI = Cfg::NI, NJ = Cfg::NJ;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wi = warp % Cfg::WI, wj = warp / Cfg::WI;
+  const int g = lane >> 2, q = lane & 3;
+  mrem = imin(mrem, Cfg::BM);
+  nrem = imin(nrem, Cfg::BN);
+  const bool al16 = ((((uintptr_t)A | (uintptr_t)B) & 15) == 0) && ((lda & 1) == 0) && ((ldb & 1) == 0);
+  const int KT = (K + BK - 1) / BK;
+
+  double acc[NJ][NI][2];
+#pragma unroll
+  for (int a = 0; a < NJ; ++a)
+#pragma unroll
+    for (int b = 0; b < NI; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  __syncthreads();  // previous user of the ring is done
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) {
+      if (al16) gemm_load_stage<Cfg, true>(smem, s, A, lda, B, ldb, K, s, mrem, nrem);
+      else gemm_load_stage<Cfg, false>(smem, s, A, lda, B, ldb, K, s, mrem, nrem);
+    }
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      int nk = kt + STAGES - 1;
+      if (nk < KT) {
+        if (al16) gemm_load_stage<Cfg, true>(smem, nk % STAGES, A, lda, B, ldb, K, nk, mrem, nrem);
+        else gemm_load_stage<Cfg, false>(smem, nk % STAGES, A, lda, B, ldb, K, nk, mrem, nrem);
+      }
+      cp_async_commit();
+    }
+    const double* sA = smem + (kt % STAGES) * Cfg::STAGE;
+    const double* sB = sA + Cfg::A_STAGE;
+    const double* pa = sA + q * Cfg::LDA_S + wi * Cfg::WTI + g;       // + k4*4*LDA_S + ni*8
+    const double* pb = sB + (wj * Cfg::WTJ + g) * Cfg::LDB_S + q;     // + nj*8*LDB_S + k4*4
+#pragma unroll
+    for (int k4 = 0; k4 < BK / 4; ++k4) {
+      double fi[NI], fj[NJ];
+#pragma unroll
+      for (int b = 0; b < NI; ++b) fi[b] = pa[k4 * 4 * Cfg::LDA_S + b * 8];
+#pragma unroll
+      for (int a = 0; a < NJ; ++a) fj[a] = pb[a * 8 * Cfg::LDB_S + k4 * 4];
+#pragma unroll
+      for (int a = 0; a < NJ; ++a)
+#pragma unroll
+        for (int b = 0; b < NI; ++b) dmma884(acc[a][b][0], acc[a][b][1], fj[a], fi[b]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: lane owns rows i..i+1 of column j for every (nj, ni) block.  Loads are batched per
+  // j-block (NI independent 16-byte loads in flight) so the tile's C traffic is not a chain of
+  // serialized round trips.
+  const bool vec = ((((uintptr_t)Cin | (uintptr_t)Cout) & 15) == 0) && ((ldcin & 1) == 0) && ((ldcout & 1) == 0);
+  const bool full = vec && mrem == Cfg::BM && nrem == Cfg::BN;
+  if (full) {
+#pragma unroll
+    for (int a = 0; a < NJ; ++a) {
+      int j = wj * Cfg::WTJ + a * 8 + g;
+      const double* ci = Cin + (int64_t)j * ldcin + wi * Cfg::WTI + 2 * q;
+      double* co = Cout + (int64_t)j * ldcout + wi * Cfg::WTI + 2 * q;
+      double2 c[NI];
+#pragma unroll
+      for (int b = 0; b < NI; ++b) c[b] = *reinterpret_cast<const double2*>(ci + b * 8);
+#pragma unroll
+      for (int b = 0; b < NI; ++b) {
+        if (alpha == 1.0) { c[b].x = fma(beta, acc[a][b][0], c[b].x); c[b].y = fma(beta, acc[a][b][1], c[b].y); }
+        else { c[b].x = alpha * c[b].x + beta * acc[a][b][0]; c[b].y = alpha * c[b].y + beta * acc[a][b][1]; }
+      }
+#pragma unroll
+      for (int b = 0; b < NI; ++b) *reinterpret_cast<double2*>(co + b * 8) = c[b];
+    }
+    return;
+  }
+#pragma unroll
+  for (int a = 0; a < NJ; ++a) {
+    int j = wj * Cfg::WTJ + a * 8 + g;
+    if (j >= nrem) continue;
+#pragma unroll
+    for (int b = 0; b < NI; ++b) {
+      int i = wi * Cfg::WTI + b * 8 + 2 * q;
+      if (i >= mrem) continue;
+      const double* ci = Cin + (int64_t)j * ldcin + i;
+      double* co = Cout + (int64_t)j * ldcout + i;
+      if (vec && i + 1 < mrem) {
+        double2 c = *reinterpret_cast<const double2*>(ci);
+        if (alpha == 1.0) { c.x = fma(beta, acc[a][b][0], c.x); c.y = fma(beta, acc[a][b][1], c.y); }
+        else { c.x = alpha * c.x + beta * acc[a][b][0]; c.y = alpha * c.y + beta * acc[a][b][1]; }
+        *reinterpret_cast<double2*>(co) = c;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (i + e < mrem) {
+            double c = ci[e];
+            c = (alpha == 1.0) ? fma(beta, acc[a][b][e], c) : alpha * c + beta * acc[a][b][e];
+            co[e] = c;
+          }
+        }
+      }
+    }
+  }
+}
+
+// A whole C := alpha*C + beta*A@B problem as a list of BM x BN tiles, column-strip major
+// (consecutive tile ids walk down the rows of one BN-wide column strip, so the k x BN strip of B
+// and the strip's prepare step are shared by neighbours in the queue).
+struct GemmProblem {
+  double* C; int64_t ldc;
+  const double* A; int64_t lda;
+  const double* B; int64_t ldb;
+  int m, n, k;
+  double alpha, beta;
+};
+
+template <class Cfg>
+__device__ __forceinline__ int gemm_num_tiles(const GemmProblem& p) {
+  return ((p.m + Cfg::BM - 1) / Cfg::BM) * ((p.n + Cfg::BN - 1) / Cfg::BN);
+}
+
+template <class Cfg>
+__device__ __forceinline__ void gemm_run_tile(const GemmProblem& p, int t, double* smem) {
+  const int tm_count = (p.m + Cfg::BM - 1) / Cfg::BM;
+  const int tm = t % tm_count, tn = t / tm_count;
+  const int i0 = tm * Cfg::BM, j0 = tn * Cfg::BN;
+  double* c = p.C + (int64_t)j0 * p.ldc + i0;
+  gemm_tile<Cfg>(p.A + i0, p.lda, p.B + (int64_t)j0 * p.ldb, p.ldb, p.k, c, p.ldc, c, p.ldc,
+                 p.m - i0, p.n - j0, p.alpha, p.beta, smem);
+}
+
+}  // namespace mla
