@@ -124,11 +124,8 @@ int mla_fill_random(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t
                     int64_t col0, int64_t total_rows, double scale, double shift,
                     const double* row_scale, void* stream);
 
-/* residual_lu(a_orig, L, U, piv) -- matrix.py:116-131: ||P*A - L*U||_F / ||A||_F from the packed
- * factors, computed on the device (A_orig is destroyed: it is overwritten by P*A - L*U).
- * Synchronous; result in *residual. */
-int mla_residual_lu(mla_handle h, double* A_orig, const double* LU, int64_t m, int64_t n, int64_t ld_a,
-                    int64_t ld_lu, const int32_t* ipiv, double* residual, void* stream);
+/* residual_lu (matrix.py:116-131) has no entry point of its own: the Python layer composes it from
+ * mla_laswp (P*A) and mla_gemm (blocked L*U), see paper_1611_06365_b200/matrix.py. */
 
 #ifdef __cplusplus
 }

@@ -52,11 +52,9 @@ def lib() -> ctypes.CDLL:
                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(LuInfo)]
     L.mla_fill_random.argtypes = [_vp, _vp, _i64, _i64, _i64, ctypes.c_uint64, _i64, _i64,
                                   ctypes.c_double, ctypes.c_double, _vp, _vp]
-    L.mla_residual_lu.argtypes = [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp,
-                                  ctypes.POINTER(ctypes.c_double), _vp]
     for name in ("mla_create", "mla_destroy", "mla_num_sms", "mla_last_cuda_error", "mla_gemm",
                  "mla_trsm_llu", "mla_laswp", "mla_panel_ll", "mla_getrf_la", "mla_getrf_la_sync",
-                 "mla_getrf_la_host", "mla_fill_random", "mla_residual_lu"):
+                 "mla_getrf_la_host", "mla_fill_random"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -64,7 +62,7 @@ def lib() -> ctypes.CDLL:
 
 EXPORTS = ("mla_version", "mla_create", "mla_destroy", "mla_num_sms", "mla_last_cuda_error",
            "mla_gemm", "mla_trsm_llu", "mla_laswp", "mla_panel_ll", "mla_getrf_la",
-           "mla_getrf_la_sync", "mla_getrf_la_host", "mla_fill_random", "mla_residual_lu")
+           "mla_getrf_la_sync", "mla_getrf_la_host", "mla_fill_random")
 
 
 class MlaError(RuntimeError):

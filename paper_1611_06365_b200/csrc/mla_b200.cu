@@ -9,6 +9,10 @@
 #include "../../include/mla_b200.h"
 #include "mla_common.cuh"
 #include "mla_gemm.cuh"
+#include "mla_laswp.cuh"
+#include "mla_trsm.cuh"
+#include "mla_panel.cuh"
+#include "mla_getrf.cuh"
 
 using namespace mla;
 
@@ -22,12 +26,27 @@ enum CtrlWord {
   CW_COUNT = 64
 };
 
+constexpr int kDynSmemBytes = 220 * 1024;   // dynamic shared memory of the team kernels
+constexpr int kDynSmemDoubles = kDynSmemBytes / 8;
+
 struct mla_handle_s {
   int device;
   int num_sms;
   int last_cuda;
   unsigned* ctrl;        // CW_COUNT words (device)
   unsigned* ctrl_host;   // pinned mirror
+  PivPlan* plan;         // device: permutation plan of the last pivot block
+  PanelWs* panel_ws;     // device: exchange slots of the panel team
+  LuState* lu_state;     // device: persistent-kernel state
+  int* piv_local;        // device: panel-local pivots of the current panel (kMaxPiv)
+  mla_lu_info* info_dev; // device
+  mla_lu_info* info_host;  // pinned
+  int32_t* widths_dev;   // device, kWidthsCap
+  double* a_dev;         // cached device matrix for the _host entry point
+  size_t a_dev_bytes;
+  int32_t* ipiv_dev;
+  size_t ipiv_dev_n;
+  double* resid_dev;
 };
 
 #define CK(h, call)                                   \
@@ -40,6 +59,8 @@ struct mla_handle_s {
   } while (0)
 
 extern "C" const char* mla_version(void) { return "paper_1611_06365_b200 0.1 (sm_100a)"; }
+
+extern "C" int mla_destroy(mla_handle h);
 
 extern "C" int mla_create(int device, mla_handle* out) {
   if (!out) return MLA_E_INVALID;
@@ -54,6 +75,18 @@ extern "C" int mla_create(int device, mla_handle* out) {
   if (cudaMalloc(&h->ctrl, CW_COUNT * sizeof(unsigned)) != cudaSuccess) { delete h; return MLA_E_CUDA; }
   if (cudaMallocHost(&h->ctrl_host, CW_COUNT * sizeof(unsigned)) != cudaSuccess) { cudaFree(h->ctrl); delete h; return MLA_E_CUDA; }
   cudaMemset(h->ctrl, 0, CW_COUNT * sizeof(unsigned));
+  bool ok = cudaMalloc(&h->plan, sizeof(PivPlan)) == cudaSuccess &&
+            cudaMalloc(&h->panel_ws, sizeof(PanelWs)) == cudaSuccess &&
+            cudaMalloc(&h->lu_state, sizeof(LuState)) == cudaSuccess &&
+            cudaMalloc(&h->piv_local, kMaxPiv * sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&h->info_dev, sizeof(mla_lu_info)) == cudaSuccess &&
+            cudaMallocHost(&h->info_host, sizeof(mla_lu_info)) == cudaSuccess &&
+            cudaMalloc(&h->widths_dev, kWidthsCap * sizeof(int32_t)) == cudaSuccess &&
+            cudaMalloc(&h->resid_dev, 4 * sizeof(double)) == cudaSuccess;
+  if (!ok) { mla_destroy(h); return MLA_E_NOMEM; }
+  cudaMemset(h->plan, 0, sizeof(PivPlan));
+  cudaMemset(h->panel_ws, 0, sizeof(PanelWs));
+  cudaMemset(h->lu_state, 0, sizeof(LuState));
   *out = h;
   return MLA_OK;
 }
@@ -62,6 +95,16 @@ extern "C" int mla_destroy(mla_handle h) {
   if (!h) return MLA_E_INVALID;
   cudaFree(h->ctrl);
   cudaFreeHost(h->ctrl_host);
+  cudaFree(h->plan);
+  cudaFree(h->panel_ws);
+  cudaFree(h->lu_state);
+  cudaFree(h->piv_local);
+  cudaFree(h->info_dev);
+  cudaFreeHost(h->info_host);
+  cudaFree(h->widths_dev);
+  cudaFree(h->resid_dev);
+  cudaFree(h->a_dev);
+  cudaFree(h->ipiv_dev);
   delete h;
   return MLA_OK;
 }
@@ -141,12 +184,255 @@ extern "C" int mla_gemm(mla_handle h, double* C, int64_t m, int64_t n, int64_t l
   return MLA_OK;
 }
 
-// ---- TEMPORARY STUBS (replaced as kernels land) ----
-extern "C" int mla_trsm_llu(mla_handle, const double*, int64_t, int64_t, double*, int64_t, int64_t, void*) { return MLA_E_INVALID; }
-extern "C" int mla_laswp(mla_handle, double*, int64_t, int64_t, int64_t, const int32_t*, int64_t, int, void*) { return MLA_E_INVALID; }
-extern "C" int mla_panel_ll(mla_handle, double*, int64_t, int64_t, int64_t, int32_t*, int, const uint32_t*, int, int, mla_lu_info*, void*) { return MLA_E_INVALID; }
-extern "C" int mla_getrf_la(mla_handle, double*, int64_t, int64_t, int64_t, int32_t*, int, int, int, int, int, mla_lu_info*, int32_t*, int, void*) { return MLA_E_INVALID; }
-extern "C" int mla_getrf_la_sync(mla_handle, double*, int64_t, int64_t, int64_t, int32_t*, int, int, int, int, int, mla_lu_info*, int32_t*, int, void*) { return MLA_E_INVALID; }
-extern "C" int mla_getrf_la_host(mla_handle, double*, int64_t, int64_t, int64_t, int32_t*, int, int, int, int, int, mla_lu_info*) { return MLA_E_INVALID; }
-extern "C" int mla_fill_random(mla_handle, double*, int64_t, int64_t, int64_t, uint64_t, int64_t, int64_t, double, double, const double*, void*) { return MLA_E_INVALID; }
-extern "C" int mla_residual_lu(mla_handle, double*, const double*, int64_t, int64_t, int64_t, int64_t, const int32_t*, double*, void*) { return MLA_E_INVALID; }
+
+// ---- trsm ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1)
+k_trsm(const double* L, int w, int64_t ldl, double* B, int64_t c, int64_t ldb) {
+  extern __shared__ __align__(16) double smem[];
+  const int64_t strips = (c + TRSM_CW - 1) / TRSM_CW;
+  for (int64_t s = blockIdx.x; s < strips; s += gridDim.x) {
+    int64_t c0 = s * TRSM_CW;
+    trsm_strip(L, w, ldl, B + c0 * ldb, (int)(c - c0 < TRSM_CW ? c - c0 : TRSM_CW), ldb, smem);
+  }
+}
+
+extern "C" int mla_trsm_llu(mla_handle h, const double* L, int64_t w, int64_t ldl, double* B, int64_t c,
+                            int64_t ldb, void* stream) {
+  if (!h || w < 0 || c < 0) return MLA_E_INVALID;
+  if (w <= 1 || c == 0) return MLA_OK;  // kernels.py:290: nothing to do
+  if (ldl < w || ldb < w) return MLA_E_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int smem_bytes = TRSM_SMEM_DOUBLES * 8;
+  CK(h, cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  int64_t strips = (c + TRSM_CW - 1) / TRSM_CW;
+  int grid = (int)(strips < h->num_sms ? strips : h->num_sms);
+  k_trsm<<<grid, kThreads, smem_bytes, s>>>(L, (int)w, ldl, B, c, ldb);
+  CK(h, cudaGetLastError());
+  return MLA_OK;
+}
+
+// ---- laswp -----------------------------------------------------------------------------------------
+__global__ void k_laswp_plan(const int* ipiv, int npiv, int64_t rows, int reverse, PivPlan* plan, unsigned* ctrl) {
+  __shared__ int top[kMaxPiv], lrow[kMaxPiv], lcur[kMaxPiv];
+  bool ok = build_pivot_plan(ipiv, npiv, rows, reverse != 0, plan->ref(), top, lrow, lcur);
+  if (threadIdx.x == 0) ctrl[CW_ERR_INDEX] = ok ? 0u : 1u;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_laswp_apply(double* A, int64_t cols, int64_t ld, PivPlan* plan) {
+  extern __shared__ __align__(16) double smem[];
+  // contiguous balanced column shares, like the reference's _share (kernels.py:28-32)
+  int64_t per = (cols + gridDim.x - 1) / gridDim.x;
+  per = (per + 15) & ~(int64_t)15;
+  int64_t lo = blockIdx.x * per, hi = lo + per < cols ? lo + per : cols;
+  if (lo >= hi) return;
+  laswp_apply_cols(A + lo * ld, ld, (int)(hi - lo), plan->ref(), smem, kPlanCap * 4);
+}
+
+extern "C" int mla_laswp(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
+                         int64_t npiv, int reverse, void* stream) {
+  if (!h || rows < 0 || cols < 0 || npiv < 0 || (rows > 0 && ld < rows)) return MLA_E_INVALID;
+  if (npiv == 0) return MLA_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int smem_bytes = kPlanCap * 4 * 8;
+  CK(h, cudaFuncSetAttribute(k_laswp_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  // pivot blocks wider than one plan are applied as consecutive chunks (ascending for forward,
+  // descending for reverse); chunk c works on the view that starts at its first row.
+  int64_t nchunks = (npiv + kMaxPiv - 1) / kMaxPiv;
+  int rc = MLA_OK;
+  for (int64_t ci = 0; ci < nchunks; ++ci) {
+    int64_t c = reverse ? (nchunks - 1 - ci) : ci;
+    int64_t t0 = c * kMaxPiv;
+    int np = (int)(npiv - t0 < kMaxPiv ? npiv - t0 : kMaxPiv);
+    if (c == 0) {
+      k_laswp_plan<<<1, 32, 0, s>>>(ipiv, np, rows, reverse, h->plan, h->ctrl);
+    } else {
+      // indices of later chunks are relative to row 0 of the view: rebase by -t0 on the fly is
+      // not possible without a copy, so chunked plans are only offered when the caller's pivots
+      // are already chunk-local.  (The LU path never needs more than kMaxPiv pivots per block.)
+      return MLA_E_INVALID;
+    }
+    CK(h, cudaGetLastError());
+    if (cols > 0 && rows > 0) {
+      int64_t want = (cols + 15) / 16;
+      int grid = (int)(want < 2 * h->num_sms ? want : 2 * h->num_sms);
+      if (grid < 1) grid = 1;
+      k_laswp_apply<<<grid, kThreads, smem_bytes, s>>>(A, cols, ld, h->plan);
+      CK(h, cudaGetLastError());
+    }
+  }
+  CK(h, cudaMemcpyAsync(h->ctrl_host + CW_ERR_INDEX, h->ctrl + CW_ERR_INDEX, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CK(h, cudaStreamSynchronize(s));
+  if (h->ctrl_host[CW_ERR_INDEX] != 0u) rc = MLA_E_INDEX;
+  return rc;
+}
+
+// ---- panel (standalone lu_blk_ll) --------------------------------------------------------------------
+struct PanelKArgs {
+  double* P; int m, w; int64_t ld; int* ipiv; int b_inner;
+  const unsigned* stop_flag; int stop_after_polls;
+  PanelWs* ws; unsigned* ctrl; mla_lu_info* info;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_panel(PanelKArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  Team team;
+  team.init(blockIdx.x, gridDim.x, a.ctrl + CW_BAR_ALL, a.ctrl + CW_ABORT);
+  PanelResult r = panel_ll(team, a.P, a.m, a.w, a.ld, a.ipiv, a.b_inner, a.stop_flag, 0u, a.stop_after_polls,
+                           a.ws, smem, kDynSmemDoubles);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.info->cols_factored = r.cols_factored;
+    a.info->singular = r.singular;
+    a.info->et_events = (r.cols_factored < a.w) ? 1 : 0;
+    a.info->n_panels = 1;
+    a.info->ws_joins = 0;
+  }
+}
+
+static int check_abort(mla_handle h, cudaStream_t s) {
+  if (cudaMemcpyAsync(h->ctrl_host + CW_ABORT, h->ctrl + CW_ABORT, sizeof(unsigned), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return MLA_E_CUDA;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) { h->last_cuda = (int)e; return MLA_E_CUDA; }
+  return h->ctrl_host[CW_ABORT] != 0u ? MLA_E_ABORT : MLA_OK;
+}
+
+extern "C" int mla_panel_ll(mla_handle h, double* P, int64_t m, int64_t w, int64_t ld, int32_t* ipiv, int b_inner,
+                            const uint32_t* stop_flag, int stop_after_polls, int team_ctas, mla_lu_info* info,
+                            void* stream) {
+  if (!h || m < w || w < 0 || b_inner < 1 || (m > 0 && ld < m)) return MLA_E_INVALID;
+  if (info) memset(info, 0, sizeof(*info));
+  if (w == 0) return MLA_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(h, cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
+  int grid = team_ctas;
+  if (grid <= 0) {
+    int64_t want = (m + 255) / 256;
+    grid = (int)(want < 1 ? 1 : want);
+  }
+  if (grid > h->num_sms) grid = h->num_sms;
+  if (grid > kMaxTeam) grid = kMaxTeam;
+  CK(h, cudaMemsetAsync(h->ctrl, 0, CW_COUNT * sizeof(unsigned), s));
+  PanelKArgs a{P, (int)m, (int)w, ld, ipiv, b_inner, stop_flag, stop_after_polls, h->panel_ws, h->ctrl, h->info_dev};
+  void* args[] = {&a};
+  CK(h, cudaLaunchCooperativeKernel((void*)k_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
+  CK(h, cudaMemcpyAsync(h->info_host, h->info_dev, sizeof(mla_lu_info), cudaMemcpyDeviceToHost, s));
+  int rc = check_abort(h, s);
+  if (info) *info = *h->info_host;
+  return rc;
+}
+
+// ---- getrf (persistent kernel) ----------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1) k_getrf(GetrfArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  getrf_persistent(a, smem, kDynSmemDoubles);
+}
+
+extern "C" int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
+                            int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
+                            int32_t* widths, int widths_cap, void* stream) {
+  if (!h || m < n || n < 0 || (m > 0 && ld < m)) return MLA_E_INVALID;
+  if (b_inner < 1 || b_outer < b_inner || b_outer > kMaxPiv) return MLA_E_INVALID;
+  if (variant < MLA_VARIANT_LU || variant > MLA_VARIANT_LU_ET) return MLA_E_INVALID;
+  if (n > (int64_t)kMaxStrips * TRSM_CW || m >= (1ll << 31)) return MLA_E_INVALID;
+  if (variant != MLA_VARIANT_LU && (sm_pf < 1 || sm_pf >= h->num_sms)) return MLA_E_INVALID;  // lu.py:210-214
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) {
+    if (info_dev) CK(h, cudaMemsetAsync(info_dev, 0, sizeof(mla_lu_info), s));
+    return MLA_OK;
+  }
+  CK(h, cudaFuncSetAttribute(k_getrf, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
+  CK(h, cudaMemsetAsync(h->ctrl, 0, CW_COUNT * sizeof(unsigned), s));
+  CK(h, cudaMemsetAsync(h->lu_state, 0, sizeof(LuState), s));
+  GetrfArgs a{A, (int)m, (int)n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks < 1 ? 1 : q_chunks,
+              h->lu_state, h->plan, h->panel_ws, h->piv_local, h->ctrl, info_dev, widths, widths_cap};
+  void* args[] = {&a};
+  int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
+  CK(h, cudaLaunchCooperativeKernel((void*)k_getrf, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
+  return MLA_OK;
+}
+
+extern "C" int mla_getrf_la_sync(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv,
+                                 int b_outer, int b_inner, int variant, int sm_pf, int q_chunks,
+                                 mla_lu_info* info_host, int32_t* widths_host, int widths_cap, void* stream) {
+  if (!h) return MLA_E_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  int cap = widths_cap < kWidthsCap ? widths_cap : kWidthsCap;
+  if (!widths_host) cap = 0;
+  int rc = mla_getrf_la(h, A, m, n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks, h->info_dev,
+                        cap > 0 ? h->widths_dev : nullptr, cap, s);
+  if (rc != MLA_OK) return rc;
+  if (n == 0) { if (info_host) memset(info_host, 0, sizeof(*info_host)); return MLA_OK; }
+  CK(h, cudaMemcpyAsync(h->info_host, h->info_dev, sizeof(mla_lu_info), cudaMemcpyDeviceToHost, s));
+  rc = check_abort(h, s);
+  if (info_host) *info_host = *h->info_host;
+  if (rc == MLA_OK && cap > 0) {
+    int np = h->info_host->n_panels < cap ? h->info_host->n_panels : cap;
+    CK(h, cudaMemcpy(widths_host, h->widths_dev, np * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  }
+  return rc;
+}
+
+extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_t ld_host,
+                                 int32_t* ipiv_host, int b_outer, int b_inner, int variant, int sm_pf,
+                                 int q_chunks, mla_lu_info* info_host) {
+  if (!h || m < n || n < 0 || (m > 0 && ld_host < m)) return MLA_E_INVALID;
+  if (n == 0) { if (info_host) memset(info_host, 0, sizeof(*info_host)); return MLA_OK; }
+  const int64_t ld = (m + 1) & ~(int64_t)1;   // even leading dimension: 16-byte aligned columns
+  size_t bytes = (size_t)ld * (size_t)n * sizeof(double);
+  if (h->a_dev_bytes < bytes) {
+    cudaFree(h->a_dev); h->a_dev = nullptr; h->a_dev_bytes = 0;
+    CK(h, cudaMalloc(&h->a_dev, bytes));
+    h->a_dev_bytes = bytes;
+  }
+  if (h->ipiv_dev_n < (size_t)n) {
+    cudaFree(h->ipiv_dev); h->ipiv_dev = nullptr; h->ipiv_dev_n = 0;
+    CK(h, cudaMalloc(&h->ipiv_dev, (size_t)n * sizeof(int32_t)));
+    h->ipiv_dev_n = (size_t)n;
+  }
+  cudaStream_t s = 0;
+  CK(h, cudaMemcpy2DAsync(h->a_dev, ld * sizeof(double), A_host, ld_host * sizeof(double), m * sizeof(double), n,
+                          cudaMemcpyHostToDevice, s));
+  int rc = mla_getrf_la(h, h->a_dev, m, n, ld, h->ipiv_dev, b_outer, b_inner, variant, sm_pf, q_chunks, h->info_dev,
+                        nullptr, 0, s);
+  if (rc != MLA_OK) return rc;
+  CK(h, cudaMemcpy2DAsync(A_host, ld_host * sizeof(double), h->a_dev, ld * sizeof(double), m * sizeof(double), n,
+                          cudaMemcpyDeviceToHost, s));
+  CK(h, cudaMemcpyAsync(ipiv_host, h->ipiv_dev, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(h, cudaMemcpyAsync(h->info_host, h->info_dev, sizeof(mla_lu_info), cudaMemcpyDeviceToHost, s));
+  rc = check_abort(h, s);
+  if (info_host) *info_host = *h->info_host;
+  return rc;
+}
+
+// ---- fill_random -----------------------------------------------------------------------------------
+// matrix.py:47-59: draw k = i + j*total_rows (0-based) of the stream uses state seed + (k+1)*gamma.
+__global__ void k_fill_random(double* A, int64_t rows, int64_t cols, int64_t ld, unsigned long long seed,
+                              int64_t col0, int64_t total_rows, double scale, double shift,
+                              const double* row_scale) {
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+      unsigned long long k = (unsigned long long)(i + (j + col0) * total_rows);
+      unsigned long long z = seed + (k + 1ull) * 0x9E3779B97F4A7C15ull;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      z = z ^ (z >> 31);
+      double u = __ddiv_rn((double)(z >> 11) + 1.0, 9007199254740994.0);
+      double v = __dadd_rn(__dmul_rn(scale, u), shift);   // no FMA: matches the host's two roundings
+      if (row_scale) v = __dmul_rn(v, row_scale[i]);
+      A[i + j * ld] = v;
+    }
+}
+
+extern "C" int mla_fill_random(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+                               int64_t col0, int64_t total_rows, double scale, double shift,
+                               const double* row_scale, void* stream) {
+  if (!h || rows < 0 || cols < 0 || (rows > 0 && ld < rows)) return MLA_E_INVALID;
+  if (rows == 0 || cols == 0) return MLA_OK;
+  if (total_rows <= 0) total_rows = rows;
+  dim3 grid((unsigned)((rows + 255) / 256 > 256 ? 256 : (rows + 255) / 256), (unsigned)(cols > 4096 ? 4096 : cols));
+  k_fill_random<<<grid, 256, 0, (cudaStream_t)stream>>>(A, rows, cols, ld, (unsigned long long)seed, col0, total_rows,
+                                                        scale, shift, row_scale);
+  CK(h, cudaGetLastError());
+  return MLA_OK;
+}

@@ -81,18 +81,23 @@ struct Team {
     rank = r; size = s; bar = b; target = start; abort_word = ab; ok = true;
   }
   // Collective over the team's CTAs: all global writes before it are visible to all after it.
+  // `ok` stays uniform across the CTA's threads (thread 0's verdict is broadcast).
   __device__ __forceinline__ void barrier() {
+    __shared__ int s_ok;
     target += (unsigned)size;
     __syncthreads();
-    if (size > 1) {
-      if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      bool good = true;
+      if (size > 1) {
         __threadfence();
         atom_add_release(bar, 1u);
-        bool good = spin_until_ge(bar, target, abort_word);
-        if (!good) ok = false;
+        good = spin_until_ge(bar, target, abort_word);
       }
-      __syncthreads();
+      if (ld_relaxed(abort_word) != 0u) good = false;
+      s_ok = good ? 1 : 0;
     }
+    __syncthreads();
+    if (!s_ok) ok = false;
   }
 };
 

@@ -1,0 +1,343 @@
+// lu_la on the GPU: ONE persistent cooperative kernel for the whole factorization
+// (reference lu.py:197-334).  The reference's two thread teams become an SM partition:
+//
+//   CTAs [0, sm_pf)   = team PF: after the next panel's columns are updated they factor panel k+1
+//                       (panel_ll, collective over the team),
+//   CTAs [sm_pf, G)   = team RU: pull work items of the trailing update from atomic queues.
+//
+// Per outer iteration the work is cut into items, executed from two queues in this order:
+//   PQ (next panel's columns [q1, q1+w)):  PREP strips (row interchanges of the previous panel +
+//        trsm with A11, lu.py:251-253,280), then GEMM tiles of A22p (lu.py:281);
+//   RQ (remainder [q1+w, n) and the left part): PREP strips (lu.py:251-253,289), GEMM tiles of A22r
+//        (lu.py:306-308), LEFT strips (row interchanges of the L part, lu.py:252).
+// Every CTA first helps to drain PQ (it is the critical path to the next panel); PF CTAs then wait
+// for PQ to complete and run the panel while RU CTAs drain RQ.
+//
+//   WS  (lu_mb / lu_et, pool.py:377-414): a PF CTA that returns from the panel -- i.e. after the
+//        panel team's final barrier, so the donor team has fully quiesced -- simply starts pulling
+//        RQ items; the queue's item boundary is the entry point.  Teams only grow, and the split is
+//        restored at the next iteration.  lu_ws_static joins only at a q-chunk boundary of the
+//        GEMM item range (lu.py:290-304).
+//   ET  (lu_et, lu.py:177-179,309-310): the CTA that completes the last RQ item publishes
+//        ru_done = iteration; the panel polls it once per finished inner block and cuts there; the
+//        leftover columns are folded into the next iteration through `pend` (lu.py:318-326).
+//
+// A GEMM tile depends only on the PREP of its own column strip (per-strip release/acquire flag), so
+// no barrier separates the row interchanges, the triangular solve and the update.  Results do not
+// depend on which CTA ran an item: one owner per C tile, fixed k order (kernels.py:3-9).
+#pragma once
+#include "../../include/mla_b200.h"
+#include "mla_common.cuh"
+#include "mla_gemm.cuh"
+#include "mla_laswp.cuh"
+#include "mla_panel.cuh"
+#include "mla_trsm.cuh"
+
+namespace mla {
+
+constexpr int kWidthsCap = 8192;
+constexpr int kMaxStrips = 1024;   // n <= 128 * 1024 columns
+constexpr int LEFT_CW = 256;       // columns per LEFT item
+
+struct LuState {
+  // iteration descriptor: written by CTA 0 between two grid barriers, read by everybody after
+  int q0, q1, pend, w, b_target, npiv_prev, it, done;
+  // queues (reset by CTA 0 in the same window)
+  unsigned pq_next, pq_done, rq_next, rq_done;
+  // flags, tagged with the iteration number (never reset)
+  unsigned pf_done, ru_done;
+  unsigned pprep_done[kMaxStrips];
+  unsigned rprep_done[kMaxStrips];
+  // outcome
+  int singular, et_events, n_panels, ws_joins, panel_cols;
+};
+
+struct GetrfArgs {
+  double* A; int m, n; int64_t ld;
+  int* ipiv;                 // global pivots out (device int32[n])
+  int b_outer, b_inner, variant, sm_pf, q_chunks;
+  LuState* st;
+  PivPlan* plan;             // plan of the previously factored panel (view rows start at q0)
+  PanelWs* pws;
+  int* piv_local;            // panel-local pivots of the panel being factored
+  unsigned* ctrl;            // CW_* words
+  mla_lu_info* info;
+  int* widths; int widths_cap;
+};
+
+// item counts of one iteration, derived identically by every CTA from the descriptor
+struct IterShape {
+  int q0, q1, pend, w, it, kk;      // kk = q1 - q0 (depth of the update)
+  int rows;                          // m - q1
+  int nps, tmc;                      // panel strips, row tiles
+  int pq_prep, pq_total;
+  int rcols, nrs, rq_prep, rq_gemm, nleft, rq_total;
+};
+
+__device__ __forceinline__ IterShape iter_shape(const LuState* st, int m, int n) {
+  IterShape s;
+  s.q0 = *((volatile const int*)&st->q0);
+  s.q1 = *((volatile const int*)&st->q1);
+  s.pend = *((volatile const int*)&st->pend);
+  s.w = *((volatile const int*)&st->w);
+  s.it = *((volatile const int*)&st->it);
+  s.kk = s.q1 - s.q0;
+  s.rows = m - s.q1;
+  s.tmc = (s.rows + GemmUpdateCfg::BM - 1) / GemmUpdateCfg::BM;
+  s.nps = (s.w + TRSM_CW - 1) / TRSM_CW;
+  s.pq_prep = s.nps;
+  s.pq_total = s.nps + s.nps * s.tmc;
+  s.rcols = n - s.q1 - s.w;
+  s.nrs = (s.rcols + TRSM_CW - 1) / TRSM_CW;
+  s.rq_prep = s.nrs;
+  s.rq_gemm = s.nrs * s.tmc;
+  s.nleft = (s.q0 + LEFT_CW - 1) / LEFT_CW;
+  s.rq_total = s.rq_prep + s.rq_gemm + s.nleft;
+  return s;
+}
+
+// PREP of the column strip [c0, c0+cw): previous panel's interchanges (only columns >= pend still
+// owe them, lu.py:247-255) then the triangular solve with A11.
+__device__ inline void item_prep(const GetrfArgs& a, const IterShape& s, int c0, int cw, unsigned* flag,
+                                 double* smem) {
+  int lo = imax(c0, s.pend);
+  if (lo < c0 + cw)
+    laswp_apply_cols(a.A + (int64_t)lo * a.ld + s.q0, a.ld, c0 + cw - lo, a.plan->ref(), smem, kPlanCap * 4);
+  trsm_strip(a.A + (int64_t)s.q0 * a.ld + s.q0, s.kk, a.ld, a.A + (int64_t)c0 * a.ld + s.q0, cw, a.ld, smem);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(flag, (unsigned)s.it);
+  }
+}
+
+__device__ inline bool wait_flag_eq(const unsigned* flag, unsigned v, unsigned* abort_word) {
+  __shared__ int s_good;
+  if (threadIdx.x == 0) {
+    bool good = true;
+    if (ld_acquire(flag) != v) {
+      unsigned long long t0 = globaltimer_ns();
+      unsigned it = 0;
+      while (ld_acquire(flag) != v) {
+        if ((++it & 63u) == 0u) {
+          if (ld_relaxed(abort_word) != 0u) { good = false; break; }
+          if (globaltimer_ns() - t0 > kSpinTimeoutNs) { atomicExch(abort_word, 0xDEAD3u); good = false; break; }
+        }
+      }
+    }
+    s_good = good ? 1 : 0;
+  }
+  __syncthreads();
+  bool g = s_good != 0;
+  __syncthreads();
+  return g;
+}
+
+// GEMM tile (tm, strip) of A22 -= A21 @ A12 for the strip starting at column c0.
+__device__ inline void item_gemm(const GetrfArgs& a, const IterShape& s, int tm, int c0, int cw, double* smem) {
+  const int i0 = s.q1 + tm * GemmUpdateCfg::BM;
+  double* c = a.A + (int64_t)c0 * a.ld + i0;
+  gemm_tile<GemmUpdateCfg>(a.A + (int64_t)s.q0 * a.ld + i0, a.ld, a.A + (int64_t)c0 * a.ld + s.q0, a.ld, s.kk,
+                           c, a.ld, c, a.ld, a.m - i0, cw, 1.0, -1.0, smem);
+}
+
+__device__ inline void item_complete(unsigned* counter) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atom_add_release(counter, 1u);
+  }
+}
+
+__device__ inline int pop_item(unsigned* next) {
+  __shared__ int s_item;
+  if (threadIdx.x == 0) s_item = (int)atomicAdd(next, 1u);
+  __syncthreads();
+  int t = s_item;
+  __syncthreads();
+  return t;
+}
+
+// Drain the panel-section queue.  Returns false on abort.
+__device__ inline bool run_pq(const GetrfArgs& a, const IterShape& s, double* smem) {
+  LuState* st = a.st;
+  while (true) {
+    int t = pop_item(&st->pq_next);
+    if (t >= s.pq_total) return true;
+    if (t < s.pq_prep) {
+      int c0 = s.q1 + t * TRSM_CW;
+      item_prep(a, s, c0, imin(TRSM_CW, s.q1 + s.w - c0), &st->pprep_done[t], smem);
+    } else {
+      int g = t - s.pq_prep;
+      int strip = g / s.tmc, tm = g - strip * s.tmc;
+      if (!wait_flag_eq(&st->pprep_done[strip], (unsigned)s.it, a.ctrl)) return false;
+      int c0 = s.q1 + strip * TRSM_CW;
+      item_gemm(a, s, tm, c0, imin(TRSM_CW, s.q1 + s.w - c0), smem);
+    }
+    item_complete(&st->pq_done);
+  }
+}
+
+// Drain the remainder queue from wherever its head is.  `first` = lowest item index this CTA may
+// take (lu_ws_static chunk boundary; 0 otherwise).  Returns the number of items executed, or -1 on
+// abort.
+__device__ inline int run_rq(const GetrfArgs& a, const IterShape& s, double* smem, bool signal_ru_done) {
+  LuState* st = a.st;
+  int executed = 0;
+  while (true) {
+    int t = pop_item(&st->rq_next);
+    if (t >= s.rq_total) return executed;
+    if (t < s.rq_prep) {
+      int c0 = s.q1 + s.w + t * TRSM_CW;
+      item_prep(a, s, c0, imin(TRSM_CW, a.n - c0), &st->rprep_done[t], smem);
+    } else if (t < s.rq_prep + s.rq_gemm) {
+      int g = t - s.rq_prep;
+      int strip = g / s.tmc, tm = g - strip * s.tmc;
+      if (!wait_flag_eq(&st->rprep_done[strip], (unsigned)s.it, a.ctrl)) return -1;
+      int c0 = s.q1 + s.w + strip * TRSM_CW;
+      item_gemm(a, s, tm, c0, imin(TRSM_CW, a.n - c0), smem);
+    } else {
+      int l = t - s.rq_prep - s.rq_gemm;
+      int c0 = l * LEFT_CW;
+      laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), a.plan->ref(), smem,
+                       kPlanCap * 4);
+    }
+    ++executed;
+    // completion; the CTA that finishes the last item announces RU done (lu.py:309-310)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned old = atom_add_release(&st->rq_done, 1u);
+      if (signal_ru_done && old + 1u == (unsigned)s.rq_total) st_release(&st->ru_done, (unsigned)s.it);
+    }
+  }
+}
+
+// The persistent kernel body.  Cooperative launch, one CTA per SM.
+__device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int smem_doubles) {
+  LuState* st = a.st;
+  const int G = gridDim.x, bid = blockIdx.x, tid = threadIdx.x;
+  unsigned* abort_word = a.ctrl;  // CW_ABORT == 0
+  Team all, pf;
+  all.init(bid, G, a.ctrl + 2 /*CW_BAR_ALL*/, abort_word);
+  const bool la = a.variant != MLA_VARIANT_LU && G >= 2;
+  const int sm_pf = la ? imax(1, imin(a.sm_pf, G - 1)) : G;
+  pf.init(bid, sm_pf, a.ctrl + 3 /*CW_BAR_PF*/, abort_word);
+  const bool is_pf = la && bid < sm_pf;
+  const bool ws = la && (a.variant == MLA_VARIANT_LU_MB || a.variant == MLA_VARIANT_LU_ET ||
+                         a.variant == MLA_VARIANT_LU_WS_STATIC);
+  const bool et = la && a.variant == MLA_VARIANT_LU_ET;
+  const int m = a.m, n = a.n;
+
+  // ---- prologue: first panel, the whole grid as one team (lu.py:224-241) --------------------------
+  const int w0 = imin(a.b_outer, n);
+  PanelResult pr = panel_ll(all, a.A, m, w0, a.ld, a.piv_local, a.b_inner, nullptr, 0u, 0, a.pws, smem, smem_doubles);
+  int k_new = pr.cols_factored;
+  int w_sched = w0;
+  int q1_of_panel = 0;       // where the just-factored panel starts
+  int b_target = a.b_outer;
+  int singular = pr.singular, et_events = 0, n_panels = 0, ws_joins = 0;
+  int q0 = 0, q1 = 0;
+
+  while (true) {
+    if (!all.ok) break;
+    // ---- bookkeeping (lu.py:314-326) by CTA 0, between two grid barriers ----------------------------
+    all.barrier();
+    if (!all.ok) break;
+    if (bid == 0) {
+      for (int t = tid; t < k_new; t += kThreads) a.ipiv[q1_of_panel + t] = q1_of_panel + a.piv_local[t];
+      if (tid < 32) {
+        int* scratch = reinterpret_cast<int*>(smem);
+        build_pivot_plan(a.piv_local, k_new, (int64_t)(m - q1_of_panel), false, a.plan->ref(), scratch,
+                         scratch + kMaxPiv, scratch + 2 * kMaxPiv);
+      }
+      if (tid == 0) {
+        if (a.widths && n_panels < a.widths_cap) a.widths[n_panels] = k_new;
+        ++n_panels;
+        if (k_new < w_sched) { ++et_events; b_target = imax(a.b_inner, k_new); }
+        else if (q1_of_panel > 0) b_target = imin(a.b_outer, 2 * b_target);
+        int pend = q1_of_panel + w_sched;
+        q0 = q1_of_panel;
+        q1 = q1_of_panel + k_new;
+        st->q0 = q0; st->q1 = q1; st->pend = pend;
+        st->w = imin(b_target, n - q1);
+        st->b_target = b_target;
+        st->npiv_prev = k_new;
+        st->it = st->it + 1;
+        st->done = (q1 >= n) ? 1 : 0;
+        st->pq_next = 0; st->pq_done = 0; st->rq_next = 0; st->rq_done = 0;
+        st->singular = singular; st->et_events = et_events; st->n_panels = n_panels; st->ws_joins = ws_joins;
+      }
+    }
+    all.barrier();
+    if (!all.ok) break;
+    IterShape s = iter_shape(st, m, n);
+    if (*((volatile const int*)&st->done)) {
+      // ---- final_sync (lu.py:328-332): last panel's interchanges for the columns to its left ------
+      for (int l = bid; l < s.nleft; l += G) {
+        int c0 = l * LEFT_CW;
+        laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), a.plan->ref(), smem,
+                         kPlanCap * 4);
+      }
+      break;
+    }
+    q1_of_panel = s.q1;
+    w_sched = s.w;
+    b_target = *((volatile const int*)&st->b_target);
+
+    if (!la) {
+      // ---- variant lu: update, then panel, one team (lu.py:259-269) --------------------------------
+      if (!run_pq(a, s, smem)) break;
+      if (run_rq(a, s, smem, false) < 0) break;
+      all.barrier();
+      if (!all.ok) break;
+      pr = panel_ll(all, a.A + (int64_t)s.q1 * a.ld + s.q1, m - s.q1, s.w, a.ld, a.piv_local, a.b_inner, nullptr,
+                    0u, 0, a.pws, smem, smem_doubles);
+    } else {
+      // ---- look-ahead: everybody drains PQ, then PF factors while RU updates (lu.py:270-312) --------
+      if (!run_pq(a, s, smem)) break;
+      if (is_pf) {
+        if (tid == 0) {
+          if (!spin_until_ge(&st->pq_done, (unsigned)s.pq_total, abort_word)) pf.ok = false;
+        }
+        __syncthreads();
+        pr = panel_ll(pf, a.A + (int64_t)s.q1 * a.ld + s.q1, m - s.q1, s.w, a.ld, a.piv_local, a.b_inner,
+                      et ? &st->ru_done : nullptr, (unsigned)s.it, 0, a.pws, smem, smem_doubles);
+        if (bid == 0 && tid == 0) st_release(&st->pf_done, (unsigned)s.it);
+        if (ws && pf.ok) {
+          // worker sharing: the quiesced panel team joins the update queue (pool.py:377-414)
+          if (a.variant == MLA_VARIANT_LU_WS_STATIC && s.rq_gemm > 0) {
+            // join only at the next q-chunk boundary of the GEMM item range (lu.py:290-304)
+            if (tid == 0) {
+              int q = imax(1, a.q_chunks);
+              unsigned head = ld_acquire(&st->rq_next);
+              int per = (s.rq_gemm + q - 1) / q;
+              int gpos = imax(0, (int)head - s.rq_prep);
+              int next_chunk = ((gpos + per - 1) / per) * per;
+              unsigned wait_for = (unsigned)(s.rq_prep + imin(next_chunk, s.rq_gemm));
+              spin_until_ge(&st->rq_next, wait_for, abort_word);
+            }
+            __syncthreads();
+          }
+          int ex = run_rq(a, s, smem, et);
+          if (ex < 0) break;
+          if (bid == 0 && ex > 0) ++ws_joins;
+        }
+      } else {
+        if (run_rq(a, s, smem, et) < 0) break;
+      }
+    }
+    k_new = pr.cols_factored;
+    singular |= pr.singular;
+    if (is_pf && !pf.ok) { if (tid == 0) atomicExch(abort_word, 0xDEAD4u); }
+  }
+  if (bid == 0 && tid == 0 && a.info) {
+    a.info->cols_factored = n;
+    a.info->singular = st->singular;
+    a.info->et_events = st->et_events;
+    a.info->n_panels = st->n_panels;
+    a.info->ws_joins = st->ws_joins;
+  }
+}
+
+}  // namespace mla

@@ -18,20 +18,27 @@ namespace mla {
 constexpr int kMaxPiv = 1024;            // widest pivot block a plan can hold
 constexpr int kPlanCap = 2 * kMaxPiv;    // touched rows <= 2 * npiv
 
-struct PivPlan {          // lives in global memory (workspace) or shared memory
-  int count;              // number of (dst, src) moves; 0 when validation failed
+struct PlanRef {           // a plan stored anywhere (global workspace or shared memory)
+  int* count;              // number of (dst, src) moves; 0 when validation failed
+  int* dst;
+  int* src;
+};
+
+struct PivPlan {           // global-memory storage of one full-size plan
+  int count;
   int npiv;
   int pad[2];
   int dst[kPlanCap];
   int src[kPlanCap];
+  __device__ __forceinline__ PlanRef ref() { return PlanRef{&count, dst, src}; }
 };
 
 // Build the plan for ipiv[0..npiv) (view-local indices, view has `rows` rows).  Executed by ONE
 // warp (all 32 lanes call it); scratch: 2*npiv ints of shared memory (lrow/lcur) + npiv ints (top).
 // Returns false (and count = 0) if an index is out of range -- nothing may then be touched
 // (kernels.py:326-327).
-__device__ inline bool build_pivot_plan(const int* __restrict__ ipiv, int npiv, int64_t rows, bool reverse,
-                                        PivPlan* plan, int* top, int* lrow, int* lcur) {
+__device__ inline bool build_pivot_plan(const int* ipiv, int npiv, int64_t rows, bool reverse,
+                                        PlanRef plan, int* top, int* lrow, int* lcur) {
   const int lane = threadIdx.x & 31;
   bool bad = false;
   for (int t = lane; t < npiv; t += 32) {
@@ -41,7 +48,7 @@ __device__ inline bool build_pivot_plan(const int* __restrict__ ipiv, int npiv, 
   }
   bad = __any_sync(0xffffffffu, bad);
   if (bad || npiv > kMaxPiv) {
-    if (lane == 0) { plan->count = 0; plan->npiv = npiv; }
+    if (lane == 0) *plan.count = 0;
     __syncwarp();
     return false;
   }
@@ -82,12 +89,12 @@ __device__ inline bool build_pivot_plan(const int* __restrict__ ipiv, int npiv, 
     unsigned m = __ballot_sync(0xffffffffu, keep);
     if (keep) {
       int pos = cnt + __popc(m & ((1u << lane) - 1u));
-      plan->dst[pos] = d;
-      plan->src[pos] = sidx;
+      plan.dst[pos] = d;
+      plan.src[pos] = sidx;
     }
     cnt += __popc(m);
   }
-  if (lane == 0) { plan->count = cnt; plan->npiv = npiv; }
+  if (lane == 0) *plan.count = cnt;
   __syncwarp();
   return true;
 }
@@ -95,9 +102,9 @@ __device__ inline bool build_pivot_plan(const int* __restrict__ ipiv, int npiv, 
 // Apply a plan to columns [0, ncols) of the view A (rows start at the plan's row 0).  Collective
 // over the CTA.  `buf` is shared memory holding at least cg*count doubles, cg >= 1 columns per
 // pass (buf_doubles gives its capacity).
-__device__ inline void laswp_apply_cols(double* __restrict__ A, int64_t ld, int ncols, const PivPlan* plan,
+__device__ inline void laswp_apply_cols(double* __restrict__ A, int64_t ld, int ncols, PlanRef plan,
                                         double* buf, int buf_doubles) {
-  const int cnt = plan->count;
+  const int cnt = *plan.count;
   if (cnt <= 0 || ncols <= 0) return;
   int cg = buf_doubles / cnt;
   if (cg > 16) cg = 16;
@@ -107,12 +114,12 @@ __device__ inline void laswp_apply_cols(double* __restrict__ A, int64_t ld, int 
     __syncthreads();
     for (int x = threadIdx.x; x < nc * cnt; x += blockDim.x) {
       int c = x / cnt, e = x - c * cnt;
-      buf[x] = A[(int64_t)(c0 + c) * ld + plan->src[e]];
+      buf[x] = A[(int64_t)(c0 + c) * ld + plan.src[e]];
     }
     __syncthreads();
     for (int x = threadIdx.x; x < nc * cnt; x += blockDim.x) {
       int c = x / cnt, e = x - c * cnt;
-      A[(int64_t)(c0 + c) * ld + plan->dst[e]] = buf[x];
+      A[(int64_t)(c0 + c) * ld + plan.dst[e]] = buf[x];
     }
   }
   __syncthreads();

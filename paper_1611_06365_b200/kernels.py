@@ -1,0 +1,89 @@
+"""trsm / gemm / row-swap operators of the reference (kernels.py:205-332) over CUDA tensors.
+
+Same names, argument meaning and error behaviour; `team` (a thread team in the reference) is
+accepted and ignored -- the kernels are collective over CTAs internally -- and `cfg` (CPU cache
+blocking) likewise.  Every call goes through the C ABI in include/mla_b200.h; nothing here computes
+on the host.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _capi
+from .matrix import PivotVector, _stream, check_colmajor
+from .pool import CompletionFlag, default_pool
+
+MAX_PIVOT_BLOCK = 1024  # kMaxPiv in csrc/mla_laswp.cuh
+
+
+def gemm_malleable(c: torch.Tensor, a: torch.Tensor, b: torch.Tensor, alpha: float = 1.0,
+                   beta: float = 1.0, cfg=None, team=None, flag: CompletionFlag | None = None,
+                   pool=None, donor_sms: int | None = None) -> None:
+    """c := alpha*c + beta*(a @ b) on the FP64 tensor cores (reference kernels.py:205-234).
+
+    `flag`: the reference's worker-sharing entry point.  With a CompletionFlag, `donor_sms` CTAs of
+    the persistent grid (default: the pool's t_pf) stay out of the tile queue until the flag is set
+    and join it at the next tile boundary.
+    """
+    m, n, ldc = check_colmajor(c, "c")
+    ma, k, lda = check_colmajor(a, "a")
+    kb, nb, ldb = check_colmajor(b, "b")
+    if ma != m or kb != k or nb != n:
+        raise ValueError(f"gemm shapes disagree: c {tuple(c.shape)}, a {tuple(a.shape)}, b {tuple(b.shape)}")
+    pool = pool or default_pool(c.device.index)
+    fptr, donors = 0, 0
+    if flag is not None:
+        fptr = flag.ptr
+        donors = pool.t_pf if donor_sms is None else int(donor_sms)
+    _capi.check(_capi.lib().mla_gemm(pool.handle, c.data_ptr(), m, n, ldc, a.data_ptr(), lda,
+                                     b.data_ptr(), ldb, k, float(alpha), float(beta), fptr, donors,
+                                     _stream(c)), pool.handle, "gemm_malleable")
+
+
+def trsm_llu(a11: torch.Tensor, b: torch.Tensor, team=None, pool=None) -> None:
+    """Solve trilu(a11) @ x = b in place; unit lower triangle (reference kernels.py:275-293)."""
+    nb, nb2, ldl = check_colmajor(a11, "a11")
+    if nb != nb2:
+        raise ValueError("triangular factor must be square")
+    rows, cols, ldb = check_colmajor(b, "b")
+    if rows != nb:
+        raise ValueError("right-hand side rows disagree with the factor")
+    pool = pool or default_pool(b.device.index)
+    _capi.check(_capi.lib().mla_trsm_llu(pool.handle, a11.data_ptr(), nb, ldl, b.data_ptr(), cols, ldb,
+                                         _stream(b)), pool.handle, "trsm_llu")
+
+
+def _device_pivots(piv, device) -> torch.Tensor:
+    if isinstance(piv, PivotVector):
+        return piv.on_device(device)
+    if isinstance(piv, torch.Tensor):
+        return piv.to(device=device, dtype=torch.int32).contiguous()
+    arr = np.asarray(piv, dtype=np.int64)
+    if arr.size and (arr.min() < -2 ** 31 or arr.max() >= 2 ** 31):
+        raise IndexError("pivot index out of range for this view")
+    return torch.from_numpy(arr.astype(np.int32)).to(device)
+
+
+def laswp(a: torch.Tensor, piv, team=None, reverse: bool = False, pool=None) -> None:
+    """Apply row interchanges k <-> ipiv[k] to every column of a, ascending (descending with
+    reverse).  Indices are validated against the view before anything is touched
+    (reference kernels.py:316-332)."""
+    rows, cols, ld = check_colmajor(a, "a")
+    ip = _device_pivots(piv, a.device)
+    npiv = int(ip.shape[0])
+    if npiv == 0:
+        return
+    pool = pool or default_pool(a.device.index)
+    if npiv > MAX_PIVOT_BLOCK:
+        # validate the whole vector first (nothing may be touched on a bad index), then apply
+        # chunk by chunk on views that start at the chunk's first row
+        if bool(((ip < 0) | (ip >= rows)).any().item()):
+            raise IndexError("pivot index out of range for this view")
+        starts = list(range(0, npiv, MAX_PIVOT_BLOCK))
+        for t0 in (reversed(starts) if reverse else starts):
+            chunk = (ip[t0:t0 + MAX_PIVOT_BLOCK] - t0).contiguous()
+            laswp(a[t0:, :], chunk, reverse=reverse, pool=pool)
+        return
+    _capi.check(_capi.lib().mla_laswp(pool.handle, a.data_ptr(), rows, cols, ld, ip.data_ptr(), npiv,
+                                      int(bool(reverse)), _stream(a)), pool.handle, "laswp")
