@@ -124,6 +124,11 @@ int mla_fill_random(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t
                     int64_t col0, int64_t total_rows, double scale, double shift,
                     const double* row_scale, void* stream);
 
+/* Phase timers of the panel team (ns, accumulated by team rank 0): [0] trsm, [1] gemm/slab load,
+ * [2] pivot steps, [3] write-back + swaps, [4] block barrier, [5] exchange share of [2].
+ * Synchronises the device. */
+int mla_panel_profile(mla_handle h, uint64_t* out16, int reset);
+
 /* residual_lu (matrix.py:116-131) has no entry point of its own: the Python layer composes it from
  * mla_laswp (P*A) and mla_gemm (blocked L*U), see paper_1611_06365_b200/matrix.py. */
 

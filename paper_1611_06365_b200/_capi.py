@@ -52,6 +52,8 @@ def lib() -> ctypes.CDLL:
                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(LuInfo)]
     L.mla_fill_random.argtypes = [_vp, _vp, _i64, _i64, _i64, ctypes.c_uint64, _i64, _i64,
                                   ctypes.c_double, ctypes.c_double, _vp, _vp]
+    L.mla_panel_profile.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+    L.mla_panel_profile.restype = ctypes.c_int
     for name in ("mla_create", "mla_destroy", "mla_num_sms", "mla_last_cuda_error", "mla_gemm",
                  "mla_trsm_llu", "mla_laswp", "mla_panel_ll", "mla_getrf_la", "mla_getrf_la_sync",
                  "mla_getrf_la_host", "mla_fill_random"):
@@ -62,7 +64,7 @@ def lib() -> ctypes.CDLL:
 
 EXPORTS = ("mla_version", "mla_create", "mla_destroy", "mla_num_sms", "mla_last_cuda_error",
            "mla_gemm", "mla_trsm_llu", "mla_laswp", "mla_panel_ll", "mla_getrf_la",
-           "mla_getrf_la_sync", "mla_getrf_la_host", "mla_fill_random")
+           "mla_getrf_la_sync", "mla_getrf_la_host", "mla_fill_random", "mla_panel_profile")
 
 
 class MlaError(RuntimeError):

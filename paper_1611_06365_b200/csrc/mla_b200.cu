@@ -436,3 +436,12 @@ extern "C" int mla_fill_random(mla_handle h, double* A, int64_t rows, int64_t co
   CK(h, cudaGetLastError());
   return MLA_OK;
 }
+
+// ---- profiling counters of the panel team (ns, rank 0): see PanelWs::prof ---------------------------
+extern "C" int mla_panel_profile(mla_handle h, uint64_t* out16, int reset) {
+  if (!h || !out16) return MLA_E_INVALID;
+  CK(h, cudaDeviceSynchronize());
+  CK(h, cudaMemcpy(out16, h->panel_ws->prof, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (reset) CK(h, cudaMemset(h->panel_ws->prof, 0, 16 * sizeof(uint64_t)));
+  return MLA_OK;
+}

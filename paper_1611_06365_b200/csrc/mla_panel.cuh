@@ -31,20 +31,59 @@ namespace mla {
 constexpr int kMaxInner = 128;   // widest block handled by the pivot-step kernel
 constexpr int kMaxTeam = 160;    // >= SM count
 
+// Exchange words are 16 bytes {payload, tag} written and read with single 128-bit STRONG.GPU
+// transactions (st/ld.relaxed.gpu.b128), so each word validates itself through its tag and the
+// per-step exchange needs no memory fence at all.
+struct alignas(16) XUnit { unsigned long long lo, hi; };
+
 struct XSlot {                   // one CTA's published candidate for one step parity
-  double val;                    // |a| of the candidate, -1 when the CTA has no active row
-  int row;                       // panel-local row of the candidate
-  unsigned tag;                  // step sequence number, written last (release)
-  double rowvals[kMaxInner];     // the candidate row's values in the block's columns
-  double diag[kMaxInner];        // the diagonal row's values (only its owner writes them)
+  XUnit head;                    // lo = |a| of the candidate (-1: no active row); hi = row<<32 | seq
+  XUnit rv[kMaxInner];           // the candidate row's values in the block's columns; hi = seq
+  XUnit dg[kMaxInner];           // the diagonal row's values (only its owner writes them); hi = seq
 };
+
+__device__ __forceinline__ void st_b128(void* p, unsigned long long lo, unsigned long long hi) {
+  asm volatile("{\n .reg .b128 t;\n mov.b128 t, {%1, %2};\n st.relaxed.gpu.global.b128 [%0], t;\n}"
+               ::"l"(p), "l"(lo), "l"(hi) : "memory");
+}
+__device__ __forceinline__ void ld_b128(const void* p, unsigned long long& lo, unsigned long long& hi) {
+  asm volatile("{\n .reg .b128 t;\n ld.relaxed.gpu.global.b128 t, [%2];\n mov.b128 {%0, %1}, t;\n}"
+               : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
+}
+// Spin until the word's tag (low 32 bits of hi) equals seq.  Returns false on abort/timeout.
+__device__ __forceinline__ bool poll_unit(const XUnit* u, unsigned seq, unsigned* abort_word,
+                                          unsigned long long& lo, unsigned long long& hi) {
+  ld_b128(u, lo, hi);
+  if ((unsigned)hi == seq) return true;
+  unsigned long long t0 = globaltimer_ns();
+  unsigned it = 0;
+  while (true) {
+    ld_b128(u, lo, hi);
+    if ((unsigned)hi == seq) return true;
+    if ((++it & 255u) == 0u) {
+      if (ld_relaxed(abort_word) != 0u) return false;
+      if (globaltimer_ns() - t0 > kSpinTimeoutNs) { atomicExch(abort_word, 0xDEAD2u); return false; }
+    }
+  }
+}
 
 struct PanelWs {
   XSlot slots[2][kMaxTeam];
   unsigned seq;                  // last sequence number used (monotonic across panels)
   int decision;                  // ET decision broadcast by rank 0
   int pad[2];
+  unsigned long long prof[16];   // rank 0's phase times in ns: 0 trsm, 1 gemm/load, 2 pivot steps,
+                                 // 3 write-back+plan+swaps, 4 block barrier, 5 exchange part of 2
 };
+
+#define MLA_PROF(idx)                                                   \
+  do {                                                                  \
+    if (rank == 0 && tid == 0) {                                        \
+      unsigned long long now_ = globaltimer_ns();                       \
+      ws->prof[idx] += now_ - prof_t;                                   \
+      prof_t = now_;                                                    \
+    }                                                                   \
+  } while (0)
 
 struct PanelResult {
   int cols_factored;
@@ -98,6 +137,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
   unsigned seq = *((volatile unsigned*)&ws->seq);
   team.barrier();  // everybody has read seq before anybody can publish / update it
   int polls = 0;
+  unsigned long long prof_t = globaltimer_ns();
 
   int j = 0;
   while (j < w) {
@@ -110,9 +150,17 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
     }
     // ---- 1. U block -------------------------------------------------------------------------
     if (j > 0) {
-      if (rank == 0) trsm_strip(P, j, ld, P + (int64_t)j * ld, wb, ld, smem);
+      {
+        // columns of the U block are dealt in shares of >= 8 (one DMMA tile) to the first CTAs
+        int nsh = imin(T, (wb + 7) / 8);
+        int per = (((wb + nsh - 1) / nsh) + 7) & ~7;
+        int c_lo = rank * per, c_hi = imin(wb, c_lo + per);
+        if (rank < nsh && c_lo < c_hi)
+          trsm_strip(P, j, ld, P + (int64_t)(j + c_lo) * ld, c_hi - c_lo, ld, smem);
+      }
       team.barrier();
     }
+    MLA_PROF(0);
     // ---- 2. slab + gemm -----------------------------------------------------------------------
     const int R = m - j;
     int rpc = (R + T - 1) / T;
@@ -142,6 +190,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       }
     }
     __syncthreads();
+    MLA_PROF(1);
 
     // ---- 3. pivot steps -------------------------------------------------------------------------
     // candidate for column 0 of the block
@@ -154,68 +203,74 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
     for (int c = 0; c < wb; ++c) {
       const int jc = j + c;            // diagonal row / global column of this step
       ++seq;
-      XSlot* myslot = &ws->slots[seq & 1][rank];
-      // A: CTA-level reduce of the candidate
+      // A: per-warp candidates -> shared memory
       cand_warp_reduce(cv, cr);
       if (lane == 0) { sh.red_val[warp] = cv; sh.red_row[warp] = cr; }
       __syncthreads();
-      double bv = sh.red_val[0];
-      int br = sh.red_row[0];
-#pragma unroll
-      for (int k = 1; k < 8; ++k)
-        if (cand_better(sh.red_val[k], sh.red_row[k], bv, br)) { bv = sh.red_val[k]; br = sh.red_row[k]; }
-      // B: publish candidate row (+ diagonal row from its owner)
-      const bool have = bv >= 0.0;
-      if (tid < wb) {
-        if (have) myslot->rowvals[tid] = Sb[(int64_t)tid * lds + (br - r0)];
-        if (jc >= r0 && jc < r1) myslot->diag[tid] = Sb[(int64_t)tid * lds + (jc - r0)];
-      }
-      __syncthreads();
-      if (tid == 0) {
-        myslot->val = have ? bv : -1.0;
-        myslot->row = have ? br : 0x7fffffff;
-        __threadfence();
-        st_release(&myslot->tag, seq);
-      }
-      // C: poll all slots, pick the winner
-      double pv = -2.0;
-      int prow = 0x7fffffff, prank = -1;
-      if (tid < T) {
-        XSlot* s = &ws->slots[seq & 1][tid];
+      // B-E: warp 0 runs the whole exchange while the other warps wait at the next barrier
+      if (warp == 0) {
+        unsigned long long xt0 = (rank == 0 && lane == 0) ? globaltimer_ns() : 0ull;
+        XSlot* slots = ws->slots[seq & 1];
+        XSlot* myslot = &slots[rank];
+        double bv = (lane < 8) ? sh.red_val[lane] : -2.0;
+        int br = (lane < 8) ? sh.red_row[lane] : 0x7fffffff;
+        cand_warp_reduce(bv, br);
+        const bool have = bv >= 0.0;
+        const bool own_diag = (jc >= r0 && jc < r1);
+        for (int cc = lane; cc < wb; cc += 32) {
+          if (have) st_b128(&myslot->rv[cc], (unsigned long long)__double_as_longlong(Sb[(int64_t)cc * lds + (br - r0)]), seq);
+          if (own_diag) st_b128(&myslot->dg[cc], (unsigned long long)__double_as_longlong(Sb[(int64_t)cc * lds + (jc - r0)]), seq);
+        }
+        if (lane == 0)
+          st_b128(&myslot->head, (unsigned long long)__double_as_longlong(have ? bv : -1.0),
+                  ((unsigned long long)(unsigned)(have ? br : 0x7fffffff) << 32) | (unsigned long long)seq);
+        // poll every member's header
+        double pv = -2.0;
+        int prow = 0x7fffffff, prank = -1;
         bool good = true;
-        if (ld_acquire(&s->tag) != seq) {
-          unsigned long long t0 = globaltimer_ns();
-          unsigned it = 0;
-          while (ld_acquire(&s->tag) != seq) {
-            if ((++it & 63u) == 0u) {
-              if (ld_relaxed(team.abort_word) != 0u) { good = false; break; }
-              if (globaltimer_ns() - t0 > kSpinTimeoutNs) { atomicExch(team.abort_word, 0xDEAD2u); good = false; break; }
+        for (int t = lane; t < T; t += 32) {
+          unsigned long long lo, hi;
+          if (!poll_unit(&slots[t].head, seq, team.abort_word, lo, hi)) { good = false; break; }
+          double v = __longlong_as_double((long long)lo);
+          int r = (int)(hi >> 32);
+          if (cand_better(v, r, pv, prow)) { pv = v; prow = r; prank = t; }
+        }
+        double wv = pv;
+        int wr = prow;
+        cand_warp_reduce(wv, wr);
+        unsigned who = __ballot_sync(0xffffffffu, pv == wv && prow == wr && prank >= 0);
+        int wrank = __shfl_sync(0xffffffffu, prank, who ? (__ffs(who) - 1) : 0);
+        good = __all_sync(0xffffffffu, good);
+        const int p = (wv > 0.0) ? wr : jc;
+        if (good && wv > 0.0) {
+          const int drank = (jc - j) / rpc;
+          for (int cc = lane; cc < wb; cc += 32) {
+            unsigned long long lo, hi, lo2 = 0, hi2 = 0;
+            ld_b128(&slots[wrank].rv[cc], lo, hi);                 // both loads in flight together
+            if (p != jc) ld_b128(&slots[drank].dg[cc], lo2, hi2);
+            if ((unsigned)hi != seq && !poll_unit(&slots[wrank].rv[cc], seq, team.abort_word, lo, hi)) { good = false; break; }
+            double uu = __longlong_as_double((long long)lo);
+            sh.u[cc] = uu;
+            if (p != jc) {
+              if ((unsigned)hi2 != seq && !poll_unit(&slots[drank].dg[cc], seq, team.abort_word, lo2, hi2)) { good = false; break; }
+              double dd = __longlong_as_double((long long)lo2);
+              // interchange rows jc <-> p inside the block (lu.py:60-64)
+              if (own_diag) Sb[(int64_t)cc * lds + (jc - r0)] = uu;
+              if (p >= r0 && p < r1) Sb[(int64_t)cc * lds + (p - r0)] = dd;
             }
           }
+          good = __all_sync(0xffffffffu, good);
         }
-        if (good) { pv = *((volatile double*)&s->val); prow = *((volatile int*)&s->row); prank = tid; }
-      }
-      {
-        // reduce (pv, prow, prank) over the CTA
-        double v = pv; int r = prow;
-        cand_warp_reduce(v, r);
-        if (lane == 0) { sh.red_val[warp] = v; sh.red_row[warp] = r; }
-        __syncthreads();
-        if (tid == 0) {
-          double wv = sh.red_val[0]; int wr = sh.red_row[0];
-          for (int k = 1; k < 8; ++k)
-            if (cand_better(sh.red_val[k], sh.red_row[k], wv, wr)) { wv = sh.red_val[k]; wr = sh.red_row[k]; }
-          sh.win_val = wv; sh.win_row = wr;
-          sh.flag = (ld_relaxed(team.abort_word) != 0u) ? 1 : 0;
+        if (lane == 0) {
+          sh.piv[c] = p;
+          sh.win_val = wv;
+          sh.flag = good ? 0 : 1;
+          if (rank == 0) ws->prof[5] += globaltimer_ns() - xt0;
         }
-        __syncthreads();
-        if (tid < T && pv == sh.win_val && prow == sh.win_row) sh.win_rank = prank;  // unique: rows are distinct
-        __syncthreads();
       }
+      __syncthreads();
       if (sh.flag) { team.ok = false; res.cols_factored = j; return res; }
       const double wval = sh.win_val;
-      const int p = (wval > 0.0) ? sh.win_row : jc;
-      if (tid == 0) sh.piv[c] = p;
       if (!(wval > 0.0)) {
         // zero pivot column: record, flag, skip (lu.py:56-59); candidate of the next column fresh
         res.singular = 1;
@@ -225,39 +280,34 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
             double v = fabs(Sb[(int64_t)(c + 1) * lds + (i - r0)]);
             if (cand_better(v, i, cv, cr)) { cv = v; cr = i; }
           }
-        __syncthreads();
         continue;
       }
-      // D: fetch the pivot row and the old diagonal row
-      const int drank = (jc - j) / rpc;
-      if (tid < wb) {
-        sh.u[tid] = *((volatile double*)&ws->slots[seq & 1][sh.win_rank].rowvals[tid]);
-        sh.d[tid] = *((volatile double*)&ws->slots[seq & 1][drank].diag[tid]);
-      }
-      __syncthreads();
-      // E: interchange rows jc <-> p inside the block (lu.py:60-64)
-      if (p != jc && tid < wb) {
-        if (jc >= r0 && jc < r1) Sb[(int64_t)tid * lds + (jc - r0)] = sh.u[tid];
-        if (p >= r0 && p < r1) Sb[(int64_t)tid * lds + (p - r0)] = sh.d[tid];
-      }
-      __syncthreads();
-      // F: scale + rank-1 update of rows below the diagonal, search next column's maximum
+      // F: scale + rank-1 update of rows below the diagonal, search next column's maximum.
+      // Columns are processed in register chunks of 8 so the shared-memory loads of a row are in
+      // flight together instead of forming a load->fma->store chain per column.
       const double pivot = sh.u[c];
       cv = -1.0; cr = 0x7fffffff;
       for (int i = imax(r0, jc + 1) + tid; i < r1; i += kThreads) {
-        double* row = Sb + (i - r0);
-        double l = row[(int64_t)c * lds] / pivot;
+        double* __restrict__ row = Sb + (i - r0);
+        const double l = row[(int64_t)c * lds] / pivot;
         row[(int64_t)c * lds] = l;
-        if (c + 1 < wb) {
-          double x = row[(int64_t)(c + 1) * lds] - l * sh.u[c + 1];
-          row[(int64_t)(c + 1) * lds] = x;
-          double v = fabs(x);
-          if (cand_better(v, i, cv, cr)) { cv = v; cr = i; }
-          for (int cc = c + 2; cc < wb; ++cc) row[(int64_t)cc * lds] -= l * sh.u[cc];
+        for (int cb = c + 1; cb < wb; cb += 8) {
+          double x[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = (cb + e < wb) ? row[(int64_t)(cb + e) * lds] : 0.0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) if (cb + e < wb) x[e] = fma(-l, sh.u[cb + e], x[e]);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) if (cb + e < wb) row[(int64_t)(cb + e) * lds] = x[e];
+          if (cb == c + 1) {
+            double v = fabs(x[0]);
+            if (cand_better(v, i, cv, cr)) { cv = v; cr = i; }
+          }
         }
       }
-      __syncthreads();
     }
+    __syncthreads();
+    MLA_PROF(2);
     // ---- write the slab back, record pivots ------------------------------------------------------
     if (resident) {
       for (int x = tid; x < nrows * wb; x += kThreads) {
@@ -288,6 +338,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       if (h1 > l1) laswp_apply_cols(P + (int64_t)(j + wb + l1) * ld + j, ld, h1 - l1, pr, ring, RING);
     }
     j += wb;
+    MLA_PROF(3);
     // ---- 5. ET poll (rank 0 decides, everybody follows) ----------------------------------------
     bool poll_here = (j < w) && (j % b_inner == 0) && (stop_flag != nullptr || stop_after_polls > 0);
     if (poll_here && rank == 0 && tid == 0) {
@@ -301,6 +352,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
     }
     if (poll_here) ++polls;
     team.barrier();
+    MLA_PROF(4);
     if (!team.ok) { res.cols_factored = j; return res; }
     if (poll_here) {
       int dec = *((volatile int*)&ws->decision);
