@@ -1,0 +1,196 @@
+"""GPU parity tests of the whole factorization (lu_la, persistent kernel) against the CPU oracle,
+the reference's golden vectors and -- at BASELINE.json's full sizes -- golden pivots plus the
+size-independent backward-error property.  Mirrors pkg/tests/test_lu.py:173-256 and
+test_acceptance.py:78-168."""
+import os
+
+import numpy as np
+import pytest
+
+import cases
+import oracle
+from parity import BACKWARD_TOL, assert_parity, first_pivot_difference
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+EPS = float(np.finfo(np.float64).eps)
+GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+VARIANTS = ("lu", "lu_la", "lu_ws_static", "lu_mb", "lu_et")
+
+
+@pytest.fixture(scope="module")
+def mla():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1611_06365_b200 as m
+    return m
+
+
+def gen(m, n, seed):
+    return cases.uniform_pm1(oracle.fill_random, m, n, seed)
+
+
+def run_and_check(mla, a_host, b_o, b_i, variant, t_pf=None, what=""):
+    m, n = a_host.shape
+    d = mla.from_numpy(a_host)
+    r = mla.lu_la(d, mla.Policy(variant, mla.BlockConfig(b_o, b_i), t_pf=t_pf))
+    ref = a_host.copy(order="F")
+    ro = oracle.lu_la(ref, b_o, b_i, et_sched=mla.et_schedule_from(r.widths, n, b_o, b_i))
+    assert tuple(r.widths) == tuple(ro.widths), f"{what}: width schedule not replayable"
+    got = mla.to_numpy(d)
+    assert_parity(got, r.ipiv.ipiv, ref, ro.ipiv, what)
+    berr = oracle.residual_lu(a_host, got, r.ipiv.ipiv) / (max(m, n) * EPS)
+    assert berr <= BACKWARD_TOL, f"{what}: backward error {berr} n eps"
+    assert r.cols_factored == n and r.singular == ro.singular
+    assert all(w > 0 and w % b_i == 0 for w in r.et_widths)            # test_lu.py:215-223
+    assert r.et_events == len(r.et_widths) == ro.et_events
+    if variant != "lu_et":
+        assert r.et_events == 0
+    return r, got
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("n,b_o,b_i", [(100, 16, 4), (300, 64, 16), (500, 128, 32), (1000, 256, 32), (97, 32, 32)])
+def test_lu_la_vs_oracle(mla, variant, n, b_o, b_i):  # test_acceptance.py:78-104 grid (reduced)
+    run_and_check(mla, gen(n, n, 1), b_o, b_i, variant, what=f"{variant} n={n} b={b_o}/{b_i}")
+
+
+@pytest.mark.parametrize("c", cases.LA, ids=lambda c: c["name"])
+def test_lu_la_golden(mla, golden, c):
+    a = gen(c["m"], c["n"], c["seed"])
+    d = mla.from_numpy(a)
+    r = mla.lu_la(d, mla.Policy(c["variant"], mla.BlockConfig(c["b_o"], c["b_i"])))
+    assert_parity(mla.to_numpy(d), r.ipiv.ipiv, golden[c["name"] + "/lu"], golden[c["name"] + "/ipiv"], c["name"])
+
+
+def test_small_n_all_variants_equal_serial_ll(mla):  # test_lu.py:173-184 (n <= b_o)
+    a = gen(60, 48, 7)
+    ref = a.copy(order="F")
+    ro = oracle.lu_blk_ll(ref, 16)
+    for v in VARIANTS:
+        d = mla.from_numpy(a)
+        r = mla.lu_la(d, mla.Policy(v, mla.BlockConfig(64, 16)))
+        assert_parity(mla.to_numpy(d), r.ipiv.ipiv, ref, ro.ipiv, v)
+
+
+def test_bad_splits_raise(mla):  # test_lu.py:187-195, lu.py:210-214
+    a = mla.from_numpy(gen(40, 40, 1))
+    pool = mla.default_pool()
+    with pytest.raises(ValueError):
+        mla.lu_la(a, mla.Policy("lu_la", mla.BlockConfig(16, 4), t_pf=pool.t))
+    with pytest.raises(ValueError):
+        mla.lu_la(mla.alloc_matrix(3, 5), mla.Policy("lu", mla.BlockConfig(2, 1)))
+    mla.lu_la(a, mla.Policy("lu", mla.BlockConfig(16, 4), t_pf=pool.t))  # plain lu ignores the split
+
+
+def test_non_et_variants_bitwise_identical_on_gpu(mla):  # test_lu.py:198-212, acceptance 3
+    a = gen(700, 700, 4)
+    outs = []
+    for v, t_pf in (("lu", None), ("lu_la", 8), ("lu_ws_static", 24), ("lu_mb", 16), ("lu_mb", 40)):
+        d = mla.from_numpy(a)
+        r = mla.lu_la(d, mla.Policy(v, mla.BlockConfig(128, 32), t_pf=t_pf))
+        outs.append((mla.to_numpy(d), r.ipiv.ipiv))
+    for lu, piv in outs[1:]:
+        assert np.array_equal(piv, outs[0][1])
+        assert np.array_equal(lu, outs[0][0])   # one owner per tile, fixed k order (kernels.py:3-9)
+
+
+def test_tall_singular_empty_dominant(mla):  # test_lu.py:94-106, 226-244
+    run_and_check(mla, gen(300, 200, 3), 64, 16, "lu_et", what="tall 300x200")
+    run_and_check(mla, gen(900, 333, 3), 128, 32, "lu_mb", what="tall 900x333")
+    a = gen(200, 200, 2)
+    a[:, 37] = 0.0
+    r, _ = run_and_check(mla, a, 64, 16, "lu_la", what="singular")
+    assert r.singular
+    r = mla.lu_la(mla.alloc_matrix(0, 0), mla.Policy("lu", mla.BlockConfig(8, 4)))
+    assert len(r.ipiv) == 0 and not r.singular
+    n = 300
+    rng = np.random.default_rng(0)
+    a = np.asfortranarray(rng.integers(-3, 4, size=(n, n)).astype(np.float64))
+    a[np.arange(n), np.arange(n)] = 4.0 * n
+    for b_o in (256, 128):
+        d = mla.from_numpy(a)
+        r = mla.lu_la(d, mla.Policy("lu_et", mla.BlockConfig(b_o, 32)))
+        assert np.array_equal(r.ipiv.ipiv, np.arange(n))                # identity pivots
+
+
+def test_unaligned_leading_dimension_and_views(mla):
+    """Views with odd offsets / odd ld take the 8-byte staging path; canary border untouched."""
+    parent = mla.alloc_matrix(411, 333)
+    parent.fill_(-5.0)
+    a = gen(301, 299, 6)
+    view = parent[7:308, 11:310]
+    view.copy_(mla.from_numpy(a))
+    r = mla.lu_la(view, mla.Policy("lu_mb", mla.BlockConfig(64, 16)))
+    ref = a.copy(order="F")
+    ro = oracle.lu_la(ref, 64, 16)
+    host = mla.to_numpy(parent)
+    assert_parity(host[7:308, 11:310], r.ipiv.ipiv, ref, ro.ipiv, "odd view")
+    host[7:308, 11:310] = -5.0
+    assert np.all(host == -5.0)
+
+
+def test_et_fires_and_ws_joins(mla):  # acceptance 4/5: ET cuts happen; panel SMs join the update
+    a = mla.make_matrix("uniform", 3072, 0)
+    r, _ = run_and_check(mla, a, 256, 32, "lu_et", what="ET n=3072")
+    assert r.et_events > 0
+    d = mla.alloc_matrix(12288, 12288)
+    mla.fill_random(d, 0, 2.0, -1.0)
+    r = mla.lu_la(d, mla.Policy("lu_mb", mla.BlockConfig(256, 32)))
+    assert r.ws_joins > 0 and r.et_events == 0
+
+
+@pytest.mark.parametrize("c", cases.BIG, ids=lambda c: c["name"])
+def test_config_shaped_golden_pivots(mla, golden, c):  # reference-produced pivots, config generators
+    a = mla.make_matrix(c["dist"], c["n"], c["seed"])
+    for variant in ("lu", "lu_et"):
+        d = mla.from_numpy(a)
+        r = mla.lu_la(d, mla.Policy(variant, mla.BlockConfig(c["b_o"], c["b_i"])))
+        d0 = first_pivot_difference(r.ipiv.ipiv, golden[c["name"] + "/ipiv"])
+        assert d0 is None, f"{c['name']} {variant}: first differing pivot {d0}"
+        got = mla.to_numpy(d)
+        assert np.abs(np.diag(got) - golden[c["name"] + "/diag"]).max() <= 1e-10 * np.abs(golden[c["name"] + "/diag"]).max()
+
+
+def _full_config(mla, name, variant="lu_et", b=None):
+    """Full-size config on the device: golden pivots (when the fixture exists) + backward error."""
+    cfg = mla.CONFIGS[name]
+    n = cfg.n
+    b_o, b_i = (cfg.b_outer, cfg.b_inner) if b is None else (b, max(1, b // 8))
+    dev = torch.device("cuda")
+    if cfg.dist == "normal":
+        a0 = mla.from_numpy(mla.make_matrix(cfg.dist, n, cfg.seed))
+    else:
+        a0 = mla.alloc_matrix(n, n)
+        rs = torch.from_numpy(mla.workloads.row_scale_vector(n)).to(dev) if cfg.dist == "uniform_rowscaled" else None
+        mla.fill_random(a0, cfg.seed, 2.0, -1.0, row_scale=rs)
+    a = mla.alloc_matrix(n, n)
+    a.copy_(a0)
+    r = mla.lu_la(a, mla.Policy(variant, mla.BlockConfig(b_o, b_i)))
+    fix = os.path.join(GOLDEN_DIR, f"golden_{name}.npz")
+    if os.path.exists(fix):
+        g = np.load(fix)
+        d0 = first_pivot_difference(r.ipiv.ipiv, g["ipiv"])
+        assert d0 is None, f"{name}: first differing pivot {d0}"
+        diag = torch.diagonal(a).cpu().numpy()
+        assert np.abs(diag - g["diag"]).max() <= 1e-9 * np.abs(g["diag"]).max()
+    berr = mla.residual_packed(a0, a, r.ipiv) / (n * EPS)     # destroys a0
+    assert berr <= BACKWARD_TOL, f"{name}: backward error {berr} n eps"
+    return r
+
+
+def test_full_config2(mla):
+    _full_config(mla, "config2", "lu")
+    _full_config(mla, "config2", "lu_la")
+    _full_config(mla, "config2", "lu_et")
+
+
+def test_full_config3_rowscaled(mla):
+    import paper_1611_06365_b200.workloads  # noqa: F401
+    _full_config(mla, "config3", "lu_et")
+
+
+@pytest.mark.parametrize("b", [128, 256, 512, 768])
+def test_full_config4_block_sweep(mla, b):
+    _full_config(mla, "config4", "lu_et", b=b)

@@ -1,0 +1,107 @@
+"""CPU-only checks: host-side logic, workload generators, and that the C-ABI library loads and
+exports every symbol include/mla_b200.h declares (no compute calls without a GPU)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1611_06365_b200 as mla
+from paper_1611_06365_b200 import _capi
+from paper_1611_06365_b200.workloads import (CONFIGS, make_matrix, row_scale_vector,
+                                             splitmix64_uniform01)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    import __graft_entry__
+    __graft_entry__.build()
+    hdr = open(os.path.join(ROOT, "include", "mla_b200.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    declared = set(re.findall(r"\b(mla_[a-z0-9_]+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    lib = _capi.lib()
+    for name in sorted(declared):
+        assert getattr(lib, name) is not None, name
+    assert declared == set(_capi.EXPORTS), (declared ^ set(_capi.EXPORTS))
+    assert b"sm_100a" in lib.mla_version()
+
+
+def test_sass_is_blackwell_fp64_tensor_path():
+    """The shipped library carries sm_100a SASS with DMMA (FP64 tensor) and LDGSTS (cp.async)."""
+    import shutil
+    import subprocess
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not on PATH")
+    out = subprocess.run(["cuobjdump", "-sass", _capi.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "DMMA.8x8x4" in out and "LDGSTS" in out
+    assert "STG.E.128.STRONG.GPU" in out  # fence-free tagged exchange words of the panel
+
+
+def test_policy_validation_matches_reference():  # reference config.py:57-84, test_config.py
+    with pytest.raises(ValueError):
+        mla.BlockConfig(16, 32)
+    with pytest.raises(ValueError):
+        mla.BlockConfig(16, 0)
+    with pytest.raises(ValueError):
+        mla.Policy("lu_xx", mla.BlockConfig(32, 8))
+    with pytest.raises(ValueError):
+        mla.Policy("lu", mla.BlockConfig(32, 8), t_pf=0)
+    with pytest.raises(ValueError):
+        mla.Policy("lu", mla.BlockConfig(32, 8), q=0)
+    assert mla.VARIANTS == ("lu", "lu_la", "lu_ws_static", "lu_mb", "lu_et")
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        mla.SmPool()
+    with pytest.raises(ValueError):
+        mla.lu_la(torch.zeros(4, 4, dtype=torch.float64).t(), mla.Policy("lu", mla.BlockConfig(2, 1)))
+
+
+@pytest.mark.parametrize("sched", [[2, 0, 1, 0, 0, 3] + [0] * 20, [1, 1, 1, 0, 2] + [0] * 30, []])
+def test_et_schedule_roundtrip(sched):
+    """widths -> (et_widths, schedule) replays lu.py:318-323 exactly like the oracle does."""
+    n, b_o, b_i = 256, 64, 8
+    a = np.asfortranarray(make_matrix("uniform", n, 21))
+    r = oracle.lu_la(a, b_o, b_i, et_sched=sched)
+    assert sum(r.widths) == n
+    again = mla.et_schedule_from(r.widths, n, b_o, b_i)
+    b = np.asfortranarray(make_matrix("uniform", n, 21))
+    r2 = oracle.lu_la(b, b_o, b_i, et_sched=again)
+    assert r2.widths == r.widths and np.array_equal(a, b)
+    cuts = mla.et_widths_from(r.widths, n, b_o, b_i)
+    assert len(cuts) == r.et_events and all(c > 0 and c % b_i == 0 for c in cuts)
+
+
+def test_workload_generators():
+    u = splitmix64_uniform01(33, 7, 5)
+    ref = oracle.alloc(33, 7)
+    oracle.fill_random(ref, 5)
+    assert np.array_equal(u, ref)
+    a = make_matrix("uniform", 64, 0)
+    assert a.flags.f_contiguous and a.min() > -1.0 and a.max() < 1.0
+    rs = row_scale_vector(64)
+    assert rs[0] == 1.0 and np.isclose(rs[-1], 10.0 ** (-6 * 63 / 64))
+    b = make_matrix("uniform_rowscaled", 64, 0)
+    assert np.array_equal(b, a * rs[:, None])
+    c = make_matrix("normal", 32, 1)
+    assert np.array_equal(c.ravel(order="F"), np.random.default_rng(1).standard_normal(32 * 32))
+    assert set(CONFIGS) == {"config1", "config2", "config3", "config4", "config5"}
+
+
+def test_config3_pivot_distance_is_reported_not_assumed():
+    """SURVEY.md 8d caveat: the row scaling as written keeps pivots NEAR the diagonal."""
+    n = 512
+    a = np.asfortranarray(make_matrix("uniform_rowscaled", n, 2))
+    r = oracle.lu_la(a, 128, 16)
+    dist_scaled = float(np.mean(r.ipiv - np.arange(n)))
+    b = np.asfortranarray(make_matrix("normal", n, 2))
+    dist_normal = float(np.mean(oracle.lu_la(b, 128, 16).ipiv - np.arange(n)))
+    assert dist_scaled < dist_normal
