@@ -140,13 +140,38 @@ k_gemm(GemmProblem p, unsigned* ctrl, const unsigned* join_flag, int donors) {
     if (!s_tile) return;
     __syncthreads();
   }
-  while (true) {
+  // one-tile lookahead: the next tile's first k-slices are prefetched while the current tile finishes
+  auto pop = [&]() {
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(ctrl + CW_QUEUE_NEXT, 1u);
     __syncthreads();
-    const int t = s_tile;
+    int t = s_tile;
     __syncthreads();
-    if (t >= ntiles) break;
-    gemm_run_tile<GemmUpdateCfg>(p, t, smem);
+    return t;
+  };
+  int t = pop();
+  if (t >= ntiles) return;
+  TileDesc cur = gemm_tile_desc<GemmUpdateCfg>(p, t);
+  int base = 0;
+  tile_prologue<GemmUpdateCfg>(cur, base, smem);
+  while (true) {
+    int tn = pop();
+    TileDesc nxt{};
+    nxt.valid = false;
+    if (tn < ntiles) nxt = gemm_tile_desc<GemmUpdateCfg>(p, tn);
+    const bool chain = nxt.valid && tile_kt<GemmUpdateCfg>(cur) >= GemmUpdateCfg::STAGES - 1;
+    if (nxt.valid && !chain) {
+      // short-k tiles cannot be chained: run cur alone, then prime nxt from scratch
+      TileDesc none{};
+      none.valid = false;
+      tile_run<GemmUpdateCfg>(cur, none, base, smem);
+      cur = nxt;
+      base = 0;
+      tile_prologue<GemmUpdateCfg>(cur, base, smem);
+      continue;
+    }
+    base = tile_run<GemmUpdateCfg>(cur, nxt, base, smem);
+    if (!nxt.valid) break;
+    cur = nxt;
   }
 }
 

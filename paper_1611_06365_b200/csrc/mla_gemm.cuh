@@ -31,6 +31,11 @@ struct GemmCfg {
   static constexpr int SMEM_BYTES = STAGES * STAGE * 8;
   static constexpr int WTI = BM / WI, WTJ = BN / WJ;
   static constexpr int NI = WTI / 8, NJ = WTJ / 8;
+  // can the slice be issued as BK/4 equal unpredicated parts (one per k4 step)?
+  static constexpr int PARTS = BK / 4;
+  static constexpr bool FAST_OK = (kThreads % (BM / 2) == 0) && (BK % (kThreads / (BM / 2)) == 0) &&
+                                  ((BK / (kThreads / (BM / 2))) % PARTS == 0) && (kThreads % (BK / 2) == 0) &&
+                                  (BN % (kThreads / (BK / 2)) == 0) && ((BN / (kThreads / (BK / 2))) % PARTS == 0);
   static_assert(WI * WJ * 32 == kThreads, "8 warps");
   static_assert(BM % 16 == 0 && BN % 8 == 0 && WTI % 8 == 0 && WTJ % 8 == 0, "tile shape");
 };
@@ -79,21 +84,100 @@ __device__ __forceinline__ void gemm_load_stage(double* smem, int slot, const do
   }
 }
 
-// One C tile.  A: mrem x K (lda), B: K x nrem (ldb), Cin/Cout: mrem x nrem.  Cout may be shared
-// memory (generic pointer).  Collective over the CTA (256 threads); smem needs Cfg::SMEM_BYTES.
+// Fast path of gemm_load_stage: interior tile (mrem == BM, nrem == BN), whole BK slice inside K,
+// 16-byte aligned operands.  All address arithmetic is a per-thread base plus compile-time strides.
+// The slice is cut into PARTS = BK/4 parts so the main loop can issue one part per k4 step: a burst
+// of LDGSTS at the top of a k-tile would sit in the MIO queue in front of the fragment LDS.64 and
+// starve the DMMA pipe.
 template <class Cfg>
-__device__ void gemm_tile(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
-                          int64_t ldb, int K, const double* Cin, int64_t ldcin, double* Cout,
-                          int64_t ldcout, int mrem, int nrem, double alpha, double beta,
-                          double* smem) {
+__device__ __forceinline__ void gemm_load_part_fast(double* smem, int slot, const double* __restrict__ A,
+                                                    int64_t lda, const double* __restrict__ B, int64_t ldb,
+                                                    int kt, int part) {
+  double* sA = smem + slot * Cfg::STAGE;
+  double* sB = sA + Cfg::A_STAGE;
+  const int tid = threadIdx.x;
+  constexpr int PARTS = Cfg::BK / 4;
+  constexpr int ACH = Cfg::BM / 2;                 // 16-byte chunks per k-row of the A slice
+  constexpr int AROWS = kThreads / ACH;            // k-rows covered per pass
+  constexpr int APASS = Cfg::BK / AROWS;
+  const int ar = tid / ACH, ac = 2 * (tid % ACH);
+  const double* ap = A + (int64_t)(kt * Cfg::BK + ar) * lda + ac;
+  double* ad = sA + ar * Cfg::LDA_S + ac;
+#pragma unroll
+  for (int pp = 0; pp < APASS / PARTS; ++pp) {
+    const int p = part * (APASS / PARTS) + pp;
+    cp_async16(ad + p * AROWS * Cfg::LDA_S, ap + (int64_t)(p * AROWS) * lda, 16);
+  }
+  constexpr int BCH = Cfg::BK / 2;                 // chunks per column of the B slice
+  constexpr int BCOLS = kThreads / BCH;            // columns covered per pass
+  constexpr int BPASS = Cfg::BN / BCOLS;
+  const int bc = tid / BCH, bk = 2 * (tid % BCH);
+  const double* bp = B + (int64_t)bc * ldb + kt * Cfg::BK + bk;
+  double* bd = sB + bc * Cfg::LDB_S + bk;
+#pragma unroll
+  for (int pp = 0; pp < BPASS / PARTS; ++pp) {
+    const int p = part * (BPASS / PARTS) + pp;
+    cp_async16(bd + p * BCOLS * Cfg::LDB_S, bp + (int64_t)(p * BCOLS) * ldb, 16);
+  }
+}
+
+// Description of one C tile for the pipelined tile engine.
+struct TileDesc {
+  const double* A; int64_t lda;       // mrem x K
+  const double* B; int64_t ldb;       // K x nrem
+  const double* Cin; int64_t ldcin;
+  double* Cout; int64_t ldcout;       // may be shared memory (generic pointer)
+  int K, mrem, nrem;
+  double alpha, beta;
+  bool valid;
+};
+
+template <class Cfg>
+__device__ __forceinline__ int tile_kt(const TileDesc& d) { return (d.K + Cfg::BK - 1) / Cfg::BK; }
+
+// Can k-tile kt of tile d take the unpredicated fast path?
+template <class Cfg>
+__device__ __forceinline__ bool tile_fast(const TileDesc& d, int kt) {
+  if (!Cfg::FAST_OK) return false;
+  return d.valid && ((((uintptr_t)d.A | (uintptr_t)d.B) & 15) == 0) && ((d.lda & 1) == 0) && ((d.ldb & 1) == 0) &&
+         d.mrem >= Cfg::BM && d.nrem >= Cfg::BN && (kt + 1) * Cfg::BK <= d.K;
+}
+
+// Issue (and commit as one group) the loads of k-tile `kt` of tile d into ring slot `slot`; an
+// out-of-range kt or an invalid tile commits an empty group so that group accounting stays uniform.
+template <class Cfg>
+__device__ __forceinline__ void tile_issue(const TileDesc& d, int kt, int slot, double* smem) {
+  if (d.valid && kt < tile_kt<Cfg>(d)) {
+    const bool al16 = ((((uintptr_t)d.A | (uintptr_t)d.B) & 15) == 0) && ((d.lda & 1) == 0) && ((d.ldb & 1) == 0);
+    const int mrem = imin(d.mrem, Cfg::BM), nrem = imin(d.nrem, Cfg::BN);
+    if (al16)
+      gemm_load_stage<Cfg, true>(smem, slot, d.A, d.lda, d.B, d.ldb, d.K, kt, mrem, nrem);
+    else
+      gemm_load_stage<Cfg, false>(smem, slot, d.A, d.lda, d.B, d.ldb, d.K, kt, mrem, nrem);
+  }
+  cp_async_commit();
+}
+
+// Prime the ring for tile d: positions 0..STAGES-2 of its k-stream go to slots base.. .
+template <class Cfg>
+__device__ __forceinline__ void tile_prologue(const TileDesc& d, int base, double* smem) {
+  __syncthreads();  // previous user of the ring is done
+#pragma unroll
+  for (int s = 0; s < Cfg::STAGES - 1; ++s) tile_issue<Cfg>(d, s, (base + s) % Cfg::STAGES, smem);
+}
+
+// Main loop + epilogue of tile d whose first STAGES-1 k-tiles are already in flight (tile_prologue or
+// the previous tile's main loop).  While d's last k-tiles are consumed the first k-tiles of `next`
+// are prefetched into the ring, so the next tile starts without a pipeline bubble and d's epilogue
+// (C read-modify-write) overlaps next's loads.  Returns the ring base of `next`.
+template <class Cfg>
+__device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, double* smem) {
   constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES, NI = Cfg::NI, NJ = Cfg::NJ;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wi = warp % Cfg::WI, wj = warp / Cfg::WI;
   const int g = lane >> 2, q = lane & 3;
-  mrem = imin(mrem, Cfg::BM);
-  nrem = imin(nrem, Cfg::BN);
-  const bool al16 = ((((uintptr_t)A | (uintptr_t)B) & 15) == 0) && ((lda & 1) == 0) && ((ldb & 1) == 0);
-  const int KT = (K + BK - 1) / BK;
+  const int mrem = imin(d.mrem, Cfg::BM), nrem = imin(d.nrem, Cfg::BN);
+  const int KT = tile_kt<Cfg>(d);
 
   double acc[NJ][NI][2];
 #pragma unroll
@@ -101,27 +185,27 @@ __device__ void gemm_tile(const double* __restrict__ A, int64_t lda, const doubl
 #pragma unroll
     for (int b = 0; b < NI; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  __syncthreads();  // previous user of the ring is done
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) {
-      if (al16) gemm_load_stage<Cfg, true>(smem, s, A, lda, B, ldb, K, s, mrem, nrem);
-      else gemm_load_stage<Cfg, false>(smem, s, A, lda, B, ldb, K, s, mrem, nrem);
+  // Pull the C tile into L2 now: the epilogue's read-modify-write then pays L2 instead of HBM latency
+  // for each of its batches (the DMMA pipe idles during the epilogue).
+  if (KT >= 2 && __isGlobal(d.Cin)) {
+    constexpr int LPC = (Cfg::BM * 8 + 127) / 128;      // 128-byte lines per tile column
+    for (int x = tid; x < nrem * LPC; x += kThreads) {
+      int col = x / LPC, seg = x - col * LPC;
+      if (seg * 16 < mrem)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(d.Cin + (int64_t)col * d.ldcin + seg * 16));
     }
-    cp_async_commit();
   }
+
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    {
-      int nk = kt + STAGES - 1;
-      if (nk < KT) {
-        if (al16) gemm_load_stage<Cfg, true>(smem, nk % STAGES, A, lda, B, ldb, K, nk, mrem, nrem);
-        else gemm_load_stage<Cfg, false>(smem, nk % STAGES, A, lda, B, ldb, K, nk, mrem, nrem);
-      }
-      cp_async_commit();
-    }
-    const double* sA = smem + (kt % STAGES) * Cfg::STAGE;
+    const int pos = kt + STAGES - 1;
+    const int lslot = (base + pos) % STAGES;
+    const TileDesc& ld = (pos < KT) ? d : next;
+    const int lkt = (pos < KT) ? pos : pos - KT;
+    const bool lfast = tile_fast<Cfg>(ld, lkt);
+    if (!lfast) tile_issue<Cfg>(ld, lkt, lslot, smem);   // fringe / unaligned: whole slice at once
+    const double* sA = smem + ((base + kt) % STAGES) * Cfg::STAGE;
     const double* sB = sA + Cfg::A_STAGE;
     const double* pa = sA + q * Cfg::LDA_S + wi * Cfg::WTI + g;       // + k4*4*LDA_S + ni*8
     const double* pb = sB + (wj * Cfg::WTJ + g) * Cfg::LDB_S + q;     // + nj*8*LDB_S + k4*4
@@ -132,17 +216,25 @@ __device__ void gemm_tile(const double* __restrict__ A, int64_t lda, const doubl
       for (int b = 0; b < NI; ++b) fi[b] = pa[k4 * 4 * Cfg::LDA_S + b * 8];
 #pragma unroll
       for (int a = 0; a < NJ; ++a) fj[a] = pb[a * 8 * Cfg::LDB_S + k4 * 4];
+      if constexpr (Cfg::FAST_OK) {
+        if (lfast) gemm_load_part_fast<Cfg>(smem, lslot, ld.A, ld.lda, ld.B, ld.ldb, lkt, k4);
+      }
 #pragma unroll
       for (int a = 0; a < NJ; ++a)
 #pragma unroll
         for (int b = 0; b < NI; ++b) dmma884(acc[a][b][0], acc[a][b][1], fj[a], fi[b]);
     }
+    if (lfast) cp_async_commit();
   }
-  cp_async_wait<0>();
+  if (!next.valid) cp_async_wait<0>();
 
   // epilogue: lane owns rows i..i+1 of column j for every (nj, ni) block.  Loads are batched per
   // j-block (NI independent 16-byte loads in flight) so the tile's C traffic is not a chain of
   // serialized round trips.
+  const double alpha = d.alpha, beta = d.beta;
+  const double* Cin = d.Cin;
+  double* Cout = d.Cout;
+  const int64_t ldcin = d.ldcin, ldcout = d.ldcout;
   const bool vec = ((((uintptr_t)Cin | (uintptr_t)Cout) & 15) == 0) && ((ldcin & 1) == 0) && ((ldcout & 1) == 0);
   const bool full = vec && mrem == Cfg::BM && nrem == Cfg::BN;
   if (full) {
@@ -162,35 +254,50 @@ __device__ void gemm_tile(const double* __restrict__ A, int64_t lda, const doubl
 #pragma unroll
       for (int b = 0; b < NI; ++b) *reinterpret_cast<double2*>(co + b * 8) = c[b];
     }
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int a = 0; a < NJ; ++a) {
-    int j = wj * Cfg::WTJ + a * 8 + g;
-    if (j >= nrem) continue;
+    for (int a = 0; a < NJ; ++a) {
+      int j = wj * Cfg::WTJ + a * 8 + g;
+      if (j >= nrem) continue;
 #pragma unroll
-    for (int b = 0; b < NI; ++b) {
-      int i = wi * Cfg::WTI + b * 8 + 2 * q;
-      if (i >= mrem) continue;
-      const double* ci = Cin + (int64_t)j * ldcin + i;
-      double* co = Cout + (int64_t)j * ldcout + i;
-      if (vec && i + 1 < mrem) {
-        double2 c = *reinterpret_cast<const double2*>(ci);
-        if (alpha == 1.0) { c.x = fma(beta, acc[a][b][0], c.x); c.y = fma(beta, acc[a][b][1], c.y); }
-        else { c.x = alpha * c.x + beta * acc[a][b][0]; c.y = alpha * c.y + beta * acc[a][b][1]; }
-        *reinterpret_cast<double2*>(co) = c;
-      } else {
+      for (int b = 0; b < NI; ++b) {
+        int i = wi * Cfg::WTI + b * 8 + 2 * q;
+        if (i >= mrem) continue;
+        const double* ci = Cin + (int64_t)j * ldcin + i;
+        double* co = Cout + (int64_t)j * ldcout + i;
+        if (vec && i + 1 < mrem) {
+          double2 c = *reinterpret_cast<const double2*>(ci);
+          if (alpha == 1.0) { c.x = fma(beta, acc[a][b][0], c.x); c.y = fma(beta, acc[a][b][1], c.y); }
+          else { c.x = alpha * c.x + beta * acc[a][b][0]; c.y = alpha * c.y + beta * acc[a][b][1]; }
+          *reinterpret_cast<double2*>(co) = c;
+        } else {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          if (i + e < mrem) {
-            double c = ci[e];
-            c = (alpha == 1.0) ? fma(beta, acc[a][b][e], c) : alpha * c + beta * acc[a][b][e];
-            co[e] = c;
+          for (int e = 0; e < 2; ++e) {
+            if (i + e < mrem) {
+              double c = ci[e];
+              c = (alpha == 1.0) ? fma(beta, acc[a][b][e], c) : alpha * c + beta * acc[a][b][e];
+              co[e] = c;
+            }
           }
         }
       }
     }
   }
+  return (base + KT) % STAGES;
+}
+
+// One stand-alone C tile (no cross-tile prefetch).  A: mrem x K (lda), B: K x nrem (ldb),
+// Cin/Cout: mrem x nrem.  Collective over the CTA (256 threads); smem needs Cfg::SMEM_BYTES.
+template <class Cfg>
+__device__ void gemm_tile(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                          int64_t ldb, int K, const double* Cin, int64_t ldcin, double* Cout,
+                          int64_t ldcout, int mrem, int nrem, double alpha, double beta,
+                          double* smem) {
+  TileDesc d{A, lda, B, ldb, Cin, ldcin, Cout, ldcout, K, mrem, nrem, alpha, beta, true};
+  TileDesc none{};
+  none.valid = false;
+  tile_prologue<Cfg>(d, 0, smem);
+  tile_run<Cfg>(d, none, 0, smem);
 }
 
 // A whole C := alpha*C + beta*A@B problem as a list of BM x BN tiles, column-strip major
@@ -207,6 +314,16 @@ struct GemmProblem {
 template <class Cfg>
 __device__ __forceinline__ int gemm_num_tiles(const GemmProblem& p) {
   return ((p.m + Cfg::BM - 1) / Cfg::BM) * ((p.n + Cfg::BN - 1) / Cfg::BN);
+}
+
+template <class Cfg>
+__device__ __forceinline__ TileDesc gemm_tile_desc(const GemmProblem& p, int t) {
+  const int tm_count = (p.m + Cfg::BM - 1) / Cfg::BM;
+  const int tm = t % tm_count, tn = t / tm_count;
+  const int i0 = tm * Cfg::BM, j0 = tn * Cfg::BN;
+  double* c = p.C + (int64_t)j0 * p.ldc + i0;
+  return TileDesc{p.A + i0, p.lda, p.B + (int64_t)j0 * p.ldb, p.ldb, c, p.ldc, c, p.ldc,
+                  p.k, p.m - i0, p.n - j0, p.alpha, p.beta, true};
 }
 
 template <class Cfg>

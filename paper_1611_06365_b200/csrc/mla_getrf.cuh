@@ -134,19 +134,11 @@ __device__ inline bool wait_flag_eq(const unsigned* flag, unsigned v, unsigned* 
 }
 
 // GEMM tile (tm, strip) of A22 -= A21 @ A12 for the strip starting at column c0.
-__device__ inline void item_gemm(const GetrfArgs& a, const IterShape& s, int tm, int c0, int cw, double* smem) {
+__device__ __forceinline__ TileDesc item_gemm_desc(const GetrfArgs& a, const IterShape& s, int tm, int c0, int cw) {
   const int i0 = s.q1 + tm * GemmUpdateCfg::BM;
   double* c = a.A + (int64_t)c0 * a.ld + i0;
-  gemm_tile<GemmUpdateCfg>(a.A + (int64_t)s.q0 * a.ld + i0, a.ld, a.A + (int64_t)c0 * a.ld + s.q0, a.ld, s.kk,
-                           c, a.ld, c, a.ld, a.m - i0, cw, 1.0, -1.0, smem);
-}
-
-__device__ inline void item_complete(unsigned* counter) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atom_add_release(counter, 1u);
-  }
+  return TileDesc{a.A + (int64_t)s.q0 * a.ld + i0, a.ld, a.A + (int64_t)c0 * a.ld + s.q0, a.ld,
+                  c, a.ld, c, a.ld, s.kk, a.m - i0, cw, 1.0, -1.0, true};
 }
 
 __device__ inline int pop_item(unsigned* next) {
@@ -158,59 +150,92 @@ __device__ inline int pop_item(unsigned* next) {
   return t;
 }
 
-// Drain the panel-section queue.  Returns false on abort.
-__device__ inline bool run_pq(const GetrfArgs& a, const IterShape& s, double* smem) {
-  LuState* st = a.st;
-  while (true) {
-    int t = pop_item(&st->pq_next);
-    if (t >= s.pq_total) return true;
-    if (t < s.pq_prep) {
-      int c0 = s.q1 + t * TRSM_CW;
-      item_prep(a, s, c0, imin(TRSM_CW, s.q1 + s.w - c0), &st->pprep_done[t], smem);
-    } else {
-      int g = t - s.pq_prep;
-      int strip = g / s.tmc, tm = g - strip * s.tmc;
-      if (!wait_flag_eq(&st->pprep_done[strip], (unsigned)s.it, a.ctrl)) return false;
-      int c0 = s.q1 + strip * TRSM_CW;
-      item_gemm(a, s, tm, c0, imin(TRSM_CW, s.q1 + s.w - c0), smem);
-    }
-    item_complete(&st->pq_done);
-  }
+// CTA-uniform non-blocking test of a strip flag
+__device__ inline bool flag_ready(const unsigned* flag, unsigned v) {
+  __shared__ int s_rdy;
+  if (threadIdx.x == 0) s_rdy = (ld_acquire(flag) == v) ? 1 : 0;
+  __syncthreads();
+  bool r = s_rdy != 0;
+  __syncthreads();
+  return r;
 }
 
-// Drain the remainder queue from wherever its head is.  `first` = lowest item index this CTA may
-// take (lu_ws_static chunk boundary; 0 otherwise).  Returns the number of items executed, or -1 on
-// abort.
-__device__ inline int run_rq(const GetrfArgs& a, const IterShape& s, double* smem, bool signal_ru_done) {
+// Drain one of the two queues of the iteration.  which == 0: PQ (next panel's columns), 1: RQ
+// (remainder + LEFT strips).  GEMM tiles run through the pipelined tile engine with a one-item
+// lookahead: while a tile finishes, the first k-slices of the next GEMM item (if its strip is already
+// prepared) are prefetched.  Returns the number of items executed, or -1 on abort.
+__device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* smem, int which,
+                                bool signal_ru_done) {
   LuState* st = a.st;
-  int executed = 0;
-  while (true) {
-    int t = pop_item(&st->rq_next);
-    if (t >= s.rq_total) return executed;
-    if (t < s.rq_prep) {
-      int c0 = s.q1 + s.w + t * TRSM_CW;
-      item_prep(a, s, c0, imin(TRSM_CW, a.n - c0), &st->rprep_done[t], smem);
-    } else if (t < s.rq_prep + s.rq_gemm) {
-      int g = t - s.rq_prep;
-      int strip = g / s.tmc, tm = g - strip * s.tmc;
-      if (!wait_flag_eq(&st->rprep_done[strip], (unsigned)s.it, a.ctrl)) return -1;
-      int c0 = s.q1 + s.w + strip * TRSM_CW;
-      item_gemm(a, s, tm, c0, imin(TRSM_CW, a.n - c0), smem);
+  unsigned* next = which ? &st->rq_next : &st->pq_next;
+  unsigned* done = which ? &st->rq_done : &st->pq_done;
+  unsigned* flags = which ? st->rprep_done : st->pprep_done;
+  const int total = which ? s.rq_total : s.pq_total;
+  const int nprep = which ? s.rq_prep : s.pq_prep;
+  const int ngemm = which ? s.rq_gemm : (s.pq_total - s.pq_prep);
+  const int col_base = which ? (s.q1 + s.w) : s.q1;
+  const int col_end = which ? a.n : (s.q1 + s.w);
+  int executed = 0, base = 0;
+  bool primed = false;
+  int t = pop_item(next);
+  while (t < total) {
+    int tn;
+    if (t >= nprep && t < nprep + ngemm) {
+      const int g = t - nprep;
+      const int strip = g / s.tmc, tm = g - strip * s.tmc;
+      const int c0 = col_base + strip * TRSM_CW;
+      TileDesc cur = item_gemm_desc(a, s, tm, c0, imin(TRSM_CW, col_end - c0));
+      if (!primed) {
+        if (!wait_flag_eq(&flags[strip], (unsigned)s.it, a.ctrl)) return -1;
+        base = 0;
+        tile_prologue<GemmUpdateCfg>(cur, base, smem);
+      }
+      tn = pop_item(next);
+      TileDesc nxt{};
+      nxt.valid = false;
+      // chaining needs the current tile to span the whole prefetch window (KT >= STAGES-1): its
+      // prologue was issued without knowing the successor
+      if (tn < nprep + ngemm && tn >= nprep && tile_kt<GemmUpdateCfg>(cur) >= GemmUpdateCfg::STAGES - 1) {
+        const int g2 = tn - nprep;
+        const int strip2 = g2 / s.tmc, tm2 = g2 - strip2 * s.tmc;
+        if (strip2 == strip || flag_ready(&flags[strip2], (unsigned)s.it)) {
+          const int c2 = col_base + strip2 * TRSM_CW;
+          nxt = item_gemm_desc(a, s, tm2, c2, imin(TRSM_CW, col_end - c2));
+        }
+      }
+      base = tile_run<GemmUpdateCfg>(cur, nxt, base, smem);
+      primed = nxt.valid;
     } else {
-      int l = t - s.rq_prep - s.rq_gemm;
-      int c0 = l * LEFT_CW;
-      laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), a.plan->ref(), smem,
-                       kPlanCap * 4);
+      if (t < nprep) {
+        const int c0 = col_base + t * TRSM_CW;
+        item_prep(a, s, c0, imin(TRSM_CW, col_end - c0), &flags[t], smem);
+      } else {
+        const int l = t - nprep - ngemm;
+        const int c0 = l * LEFT_CW;
+        laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), a.plan->ref(), smem,
+                         kPlanCap * 4);
+      }
+      primed = false;
+      tn = pop_item(next);
     }
     ++executed;
-    // completion; the CTA that finishes the last item announces RU done (lu.py:309-310)
+    // completion; in RQ the CTA that finishes the last item announces RU done (lu.py:309-310)
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      unsigned old = atom_add_release(&st->rq_done, 1u);
-      if (signal_ru_done && old + 1u == (unsigned)s.rq_total) st_release(&st->ru_done, (unsigned)s.it);
+      unsigned old = atom_add_release(done, 1u);
+      if (which && signal_ru_done && old + 1u == (unsigned)total) st_release(&st->ru_done, (unsigned)s.it);
     }
+    t = tn;
   }
+  return executed;
+}
+
+__device__ inline bool run_pq(const GetrfArgs& a, const IterShape& s, double* smem) {
+  return run_queue(a, s, smem, 0, false) >= 0;
+}
+__device__ inline int run_rq(const GetrfArgs& a, const IterShape& s, double* smem, bool signal_ru_done) {
+  return run_queue(a, s, smem, 1, signal_ru_done);
 }
 
 // The persistent kernel body.  Cooperative launch, one CTA per SM.

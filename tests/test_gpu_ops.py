@@ -44,7 +44,8 @@ def test_fill_random_bitwise(mla, golden):  # matrix.py:44-63, test_matrix.py:81
 # ---- gemm ---------------------------------------------------------------------------------------
 
 GEMM_SHAPES = [(1, 1, 1), (7, 5, 3), (37, 29, 21), (128, 128, 32), (130, 70, 300), (517, 333, 129),
-               (256, 384, 64), (1000, 999, 257)]
+               (256, 384, 64), (1000, 999, 257), (700, 600, 24), (900, 800, 40), (2048, 2048, 64),
+               (3000, 2900, 33)]
 
 
 @pytest.mark.parametrize("m,n,k", GEMM_SHAPES)
