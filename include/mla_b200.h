@@ -87,6 +87,12 @@ int mla_trsm_llu(mla_handle h, const double* L, int64_t w, int64_t ldl, double* 
 int mla_laswp(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
               int64_t npiv, int reverse, void* stream);
 
+/* Same without the synchronous read-back of the validation result (fully asynchronous): a bad index
+ * still leaves the matrix untouched, it is just not reported.  Used by stream-ordered callers whose
+ * pivots come straight from the panel kernel (multi-GPU path). */
+int mla_laswp_async(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
+                    int64_t npiv, int reverse, void* stream);
+
 /* lu_blk_ll(a, b, ipiv, stop) -- lu.py:140-180 (panel factorization, left-looking, inner block
  * b_inner; b_inner >= w gives lu_unb, lu.py:97-103).  stop_flag (device word, nullable) is the ET
  * flag: polled once per completed inner block while columns remain; stop_after_polls > 0 instead
@@ -128,6 +134,12 @@ int mla_fill_random(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t
  * [2] pivot steps, [3] write-back + swaps, [4] block barrier, [5] exchange share of [2].
  * Synchronises the device. */
 int mla_panel_profile(mla_handle h, uint64_t* out16, int reset);
+
+/* Device trace of the last mla_getrf_la call (the GPU analogue of the reference's Tracer,
+ * trace.py:26-66): one row of 5 uint64 per outer iteration -- globaltimer ns of [0] iteration start,
+ * [1] next panel's columns updated (panel may start), [2] panel end, [3] remainder update complete,
+ * [4] scheduled width << 32 | factored width.  Returns the number of rows copied. Synchronises. */
+int mla_getrf_trace(mla_handle h, uint64_t* out, int max_rows);
 
 /* residual_lu (matrix.py:116-131) has no entry point of its own: the Python layer composes it from
  * mla_laswp (P*A) and mla_gemm (blocked L*U), see paper_1611_06365_b200/matrix.py. */

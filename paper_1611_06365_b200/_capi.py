@@ -41,6 +41,8 @@ def lib() -> ctypes.CDLL:
                            ctypes.c_double, ctypes.c_double, _vp, ctypes.c_int, _vp]
     L.mla_trsm_llu.argtypes = [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp]
     L.mla_laswp.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, ctypes.c_int, _vp]
+    L.mla_laswp_async.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, ctypes.c_int, _vp]
+    L.mla_laswp_async.restype = ctypes.c_int
     L.mla_panel_ll.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, ctypes.c_int, _vp, ctypes.c_int,
                                ctypes.c_int, ctypes.POINTER(LuInfo), _vp]
     L.mla_getrf_la.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, ctypes.c_int, ctypes.c_int,
@@ -52,6 +54,8 @@ def lib() -> ctypes.CDLL:
                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(LuInfo)]
     L.mla_fill_random.argtypes = [_vp, _vp, _i64, _i64, _i64, ctypes.c_uint64, _i64, _i64,
                                   ctypes.c_double, ctypes.c_double, _vp, _vp]
+    L.mla_getrf_trace.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+    L.mla_getrf_trace.restype = ctypes.c_int
     L.mla_panel_profile.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     L.mla_panel_profile.restype = ctypes.c_int
     for name in ("mla_create", "mla_destroy", "mla_num_sms", "mla_last_cuda_error", "mla_gemm",
@@ -64,7 +68,7 @@ def lib() -> ctypes.CDLL:
 
 EXPORTS = ("mla_version", "mla_create", "mla_destroy", "mla_num_sms", "mla_last_cuda_error",
            "mla_gemm", "mla_trsm_llu", "mla_laswp", "mla_panel_ll", "mla_getrf_la",
-           "mla_getrf_la_sync", "mla_getrf_la_host", "mla_fill_random", "mla_panel_profile")
+           "mla_getrf_la_sync", "mla_getrf_la_host", "mla_fill_random", "mla_panel_profile", "mla_getrf_trace", "mla_laswp_async")
 
 
 class MlaError(RuntimeError):

@@ -26,7 +26,7 @@ enum CtrlWord {
   CW_COUNT = 64
 };
 
-constexpr int kDynSmemBytes = 220 * 1024;   // dynamic shared memory of the team kernels
+constexpr int kDynSmemBytes = 218 * 1024;   // dynamic shared memory of the team kernels
 constexpr int kDynSmemDoubles = kDynSmemBytes / 8;
 
 struct mla_handle_s {
@@ -238,8 +238,8 @@ extern "C" int mla_trsm_llu(mla_handle h, const double* L, int64_t w, int64_t ld
 
 // ---- laswp -----------------------------------------------------------------------------------------
 __global__ void k_laswp_plan(const int* ipiv, int npiv, int64_t rows, int reverse, PivPlan* plan, unsigned* ctrl) {
-  __shared__ int top[kMaxPiv], lrow[kMaxPiv], lcur[kMaxPiv];
-  bool ok = build_pivot_plan(ipiv, npiv, rows, reverse != 0, plan->ref(), top, lrow, lcur);
+  __shared__ int top[kMaxPiv], lrow[kMaxPiv], lcur[kMaxPiv], pv[kMaxPiv];
+  bool ok = build_pivot_plan(ipiv, npiv, rows, reverse != 0, plan->ref(), top, lrow, lcur, pv);
   if (threadIdx.x == 0) ctrl[CW_ERR_INDEX] = ok ? 0u : 1u;
 }
 
@@ -254,8 +254,21 @@ k_laswp_apply(double* A, int64_t cols, int64_t ld, PivPlan* plan) {
   laswp_apply_cols(A + lo * ld, ld, (int)(hi - lo), plan->ref(), smem, kPlanCap * 4);
 }
 
+static int laswp_impl(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
+                      int64_t npiv, int reverse, void* stream, bool readback);
+
 extern "C" int mla_laswp(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
                          int64_t npiv, int reverse, void* stream) {
+  return laswp_impl(h, A, rows, cols, ld, ipiv, npiv, reverse, stream, true);
+}
+
+extern "C" int mla_laswp_async(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
+                               int64_t npiv, int reverse, void* stream) {
+  return laswp_impl(h, A, rows, cols, ld, ipiv, npiv, reverse, stream, false);
+}
+
+static int laswp_impl(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
+                      int64_t npiv, int reverse, void* stream, bool readback) {
   if (!h || rows < 0 || cols < 0 || npiv < 0 || (rows > 0 && ld < rows)) return MLA_E_INVALID;
   if (npiv == 0) return MLA_OK;
   cudaStream_t s = (cudaStream_t)stream;
@@ -286,6 +299,7 @@ extern "C" int mla_laswp(mla_handle h, double* A, int64_t rows, int64_t cols, in
       CK(h, cudaGetLastError());
     }
   }
+  if (!readback) return rc;
   CK(h, cudaMemcpyAsync(h->ctrl_host + CW_ERR_INDEX, h->ctrl + CW_ERR_INDEX, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   CK(h, cudaStreamSynchronize(s));
   if (h->ctrl_host[CW_ERR_INDEX] != 0u) rc = MLA_E_INDEX;
@@ -469,4 +483,13 @@ extern "C" int mla_panel_profile(mla_handle h, uint64_t* out16, int reset) {
   CK(h, cudaMemcpy(out16, h->panel_ws->prof, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   if (reset) CK(h, cudaMemset(h->panel_ws->prof, 0, 16 * sizeof(uint64_t)));
   return MLA_OK;
+}
+
+// ---- device trace of the last mla_getrf_la call: rows of 5 uint64 (see LuState::trace) ---------------
+extern "C" int mla_getrf_trace(mla_handle h, uint64_t* out, int max_rows) {
+  if (!h || !out || max_rows < 0) return MLA_E_INVALID;
+  CK(h, cudaDeviceSynchronize());
+  int rows = max_rows < kTraceCap ? max_rows : kTraceCap;
+  CK(h, cudaMemcpy(out, h->lu_state->trace, (size_t)rows * 5 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return rows;
 }

@@ -50,7 +50,11 @@ struct LuState {
   unsigned rprep_done[kMaxStrips];
   // outcome
   int singular, et_events, n_panels, ws_joins, panel_cols;
+  // device trace (globaltimer ns), one row per outer iteration (first kTraceCap): [0] iteration
+  // start, [1] PQ complete (panel may start), [2] panel end, [3] RQ complete, [4] width<<32|k_new
+  unsigned long long trace[1024][5];
 };
+constexpr int kTraceCap = 1024;
 
 struct GetrfArgs {
   double* A; int m, n; int64_t ld;
@@ -85,14 +89,17 @@ __device__ __forceinline__ IterShape iter_shape(const LuState* st, int m, int n)
   s.rows = m - s.q1;
   s.tmc = (s.rows + GemmUpdateCfg::BM - 1) / GemmUpdateCfg::BM;
   s.nps = (s.w + TRSM_CW - 1) / TRSM_CW;
-  s.pq_prep = s.nps;
-  s.pq_total = s.nps + s.nps * s.tmc;
   s.rcols = n - s.q1 - s.w;
   s.nrs = (s.rcols + TRSM_CW - 1) / TRSM_CW;
-  s.rq_prep = s.nrs;
+  // PQ: [panel PREP][remainder PREP][panel GEMM] -- the remainder's PREP strips depend on nothing
+  // and fill the time the panel GEMM tiles would otherwise spend waiting for the panel PREP.
+  s.pq_prep = s.nps + s.nrs;
+  s.pq_total = s.pq_prep + s.nps * s.tmc;
+  // RQ: [remainder GEMM][LEFT]
+  s.rq_prep = 0;
   s.rq_gemm = s.nrs * s.tmc;
   s.nleft = (s.q0 + LEFT_CW - 1) / LEFT_CW;
-  s.rq_total = s.rq_prep + s.rq_gemm + s.nleft;
+  s.rq_total = s.rq_gemm + s.nleft;
   return s;
 }
 
@@ -169,10 +176,10 @@ __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* 
   LuState* st = a.st;
   unsigned* next = which ? &st->rq_next : &st->pq_next;
   unsigned* done = which ? &st->rq_done : &st->pq_done;
-  unsigned* flags = which ? st->rprep_done : st->pprep_done;
+  unsigned* flags = which ? st->rprep_done : st->pprep_done;   // flags the GEMM tiles of this queue wait on
   const int total = which ? s.rq_total : s.pq_total;
-  const int nprep = which ? s.rq_prep : s.pq_prep;
-  const int ngemm = which ? s.rq_gemm : (s.pq_total - s.pq_prep);
+  const int nprep = which ? 0 : s.pq_prep;
+  const int ngemm = which ? s.rq_gemm : s.nps * s.tmc;
   const int col_base = which ? (s.q1 + s.w) : s.q1;
   const int col_end = which ? a.n : (s.q1 + s.w);
   int executed = 0, base = 0;
@@ -207,8 +214,15 @@ __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* 
       primed = nxt.valid;
     } else {
       if (t < nprep) {
-        const int c0 = col_base + t * TRSM_CW;
-        item_prep(a, s, c0, imin(TRSM_CW, col_end - c0), &flags[t], smem);
+        // PQ only: panel strips first, then the remainder's strips
+        if (t < s.nps) {
+          const int c0 = s.q1 + t * TRSM_CW;
+          item_prep(a, s, c0, imin(TRSM_CW, s.q1 + s.w - c0), &st->pprep_done[t], smem);
+        } else {
+          const int r = t - s.nps;
+          const int c0 = s.q1 + s.w + r * TRSM_CW;
+          item_prep(a, s, c0, imin(TRSM_CW, a.n - c0), &st->rprep_done[r], smem);
+        }
       } else {
         const int l = t - nprep - ngemm;
         const int c0 = l * LEFT_CW;
@@ -224,7 +238,10 @@ __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* 
     if (threadIdx.x == 0) {
       __threadfence();
       unsigned old = atom_add_release(done, 1u);
-      if (which && signal_ru_done && old + 1u == (unsigned)total) st_release(&st->ru_done, (unsigned)s.it);
+      if (which && old + 1u == (unsigned)total) {
+        if (signal_ru_done) st_release(&st->ru_done, (unsigned)s.it);
+        if (s.it <= kTraceCap) st->trace[s.it - 1][3] = globaltimer_ns();
+      }
     }
     t = tn;
   }
@@ -274,7 +291,7 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
       if (tid < 32) {
         int* scratch = reinterpret_cast<int*>(smem);
         build_pivot_plan(a.piv_local, k_new, (int64_t)(m - q1_of_panel), false, a.plan->ref(), scratch,
-                         scratch + kMaxPiv, scratch + 2 * kMaxPiv);
+                         scratch + kMaxPiv, scratch + 2 * kMaxPiv, scratch + 3 * kMaxPiv);
       }
       if (tid == 0) {
         if (a.widths && n_panels < a.widths_cap) a.widths[n_panels] = k_new;
@@ -309,6 +326,8 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
     q1_of_panel = s.q1;
     w_sched = s.w;
     b_target = *((volatile const int*)&st->b_target);
+    const bool tr = s.it <= kTraceCap;
+    if (tr && bid == 0 && tid == 0) st->trace[s.it - 1][0] = globaltimer_ns();
 
     if (!la) {
       // ---- variant lu: update, then panel, one team (lu.py:259-269) --------------------------------
@@ -326,9 +345,16 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
           if (!spin_until_ge(&st->pq_done, (unsigned)s.pq_total, abort_word)) pf.ok = false;
         }
         __syncthreads();
+        if (tr && bid == 0 && tid == 0) st->trace[s.it - 1][1] = globaltimer_ns();
         pr = panel_ll(pf, a.A + (int64_t)s.q1 * a.ld + s.q1, m - s.q1, s.w, a.ld, a.piv_local, a.b_inner,
                       et ? &st->ru_done : nullptr, (unsigned)s.it, 0, a.pws, smem, smem_doubles);
-        if (bid == 0 && tid == 0) st_release(&st->pf_done, (unsigned)s.it);
+        if (bid == 0 && tid == 0) {
+          st_release(&st->pf_done, (unsigned)s.it);
+          if (tr) {
+            st->trace[s.it - 1][2] = globaltimer_ns();
+            st->trace[s.it - 1][4] = ((unsigned long long)s.w << 32) | (unsigned)pr.cols_factored;
+          }
+        }
         if (ws && pf.ok) {
           // worker sharing: the quiesced panel team joins the update queue (pool.py:377-414)
           if (a.variant == MLA_VARIANT_LU_WS_STATIC && s.rq_gemm > 0) {

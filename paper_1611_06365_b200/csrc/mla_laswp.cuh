@@ -34,17 +34,20 @@ struct PivPlan {           // global-memory storage of one full-size plan
 };
 
 // Build the plan for ipiv[0..npiv) (view-local indices, view has `rows` rows).  Executed by ONE
-// warp (all 32 lanes call it); scratch: 2*npiv ints of shared memory (lrow/lcur) + npiv ints (top).
+// warp (all 32 lanes call it); scratch: 4 arrays of npiv ints of shared memory (top/lrow/lcur/pv).
 // Returns false (and count = 0) if an index is out of range -- nothing may then be touched
 // (kernels.py:326-327).
 __device__ inline bool build_pivot_plan(const int* ipiv, int npiv, int64_t rows, bool reverse,
-                                        PlanRef plan, int* top, int* lrow, int* lcur) {
+                                        PlanRef plan, int* top, int* lrow, int* lcur, int* pv) {
   const int lane = threadIdx.x & 31;
   bool bad = false;
-  for (int t = lane; t < npiv; t += 32) {
+  // the pivots are copied to shared scratch first: the simulation below is a chain of npiv
+  // dependent steps and must not pay a global-memory round trip per step
+  for (int t = lane; t < npiv && t < kMaxPiv; t += 32) {
     int p = ipiv[t];
     if (p < 0 || (int64_t)p >= rows) bad = true;
     top[t] = t;
+    pv[t] = p;
   }
   bad = __any_sync(0xffffffffu, bad);
   if (bad || npiv > kMaxPiv) {
@@ -56,7 +59,7 @@ __device__ inline bool build_pivot_plan(const int* ipiv, int npiv, int64_t rows,
   int nlow = 0;  // entries in the lower list (uniform across lanes)
   for (int s = 0; s < npiv; ++s) {
     const int t = reverse ? (npiv - 1 - s) : s;
-    const int p = ipiv[t];
+    const int p = pv[t];
     if (p == t) continue;
     if (p < npiv) {
       if (lane == 0) { int a = top[t]; top[t] = top[p]; top[p] = a; }

@@ -100,7 +100,7 @@ struct PanelShared {
   int plan_count;
   int plan_dst[2 * kMaxInner];
   int plan_src[2 * kMaxInner];
-  int plan_top[kMaxInner], plan_lrow[kMaxInner], plan_lcur[kMaxInner];
+  int plan_top[kMaxInner], plan_lrow[kMaxInner], plan_lcur[kMaxInner], plan_pv[kMaxInner];
   int win_rank, win_row;
   double win_val;
   int flag;
@@ -324,7 +324,8 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
     if (w - wb > 0) {
       if (warp == 0) {
         PlanRef pr{&sh.plan_count, sh.plan_dst, sh.plan_src};
-        build_pivot_plan(sh.piv_rel, wb, (int64_t)(m - j), false, pr, sh.plan_top, sh.plan_lrow, sh.plan_lcur);
+        build_pivot_plan(sh.piv_rel, wb, (int64_t)(m - j), false, pr, sh.plan_top, sh.plan_lrow, sh.plan_lcur,
+                         sh.plan_pv);
       }
       __syncthreads();
       PlanRef pr{&sh.plan_count, sh.plan_dst, sh.plan_src};

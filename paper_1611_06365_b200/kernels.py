@@ -65,7 +65,7 @@ def _device_pivots(piv, device) -> torch.Tensor:
     return torch.from_numpy(arr.astype(np.int32)).to(device)
 
 
-def laswp(a: torch.Tensor, piv, team=None, reverse: bool = False, pool=None) -> None:
+def laswp(a: torch.Tensor, piv, team=None, reverse: bool = False, pool=None, check: bool = True) -> None:
     """Apply row interchanges k <-> ipiv[k] to every column of a, ascending (descending with
     reverse).  Indices are validated against the view before anything is touched
     (reference kernels.py:316-332)."""
@@ -85,5 +85,6 @@ def laswp(a: torch.Tensor, piv, team=None, reverse: bool = False, pool=None) -> 
             chunk = (ip[t0:t0 + MAX_PIVOT_BLOCK] - t0).contiguous()
             laswp(a[t0:, :], chunk, reverse=reverse, pool=pool)
         return
-    _capi.check(_capi.lib().mla_laswp(pool.handle, a.data_ptr(), rows, cols, ld, ip.data_ptr(), npiv,
-                                      int(bool(reverse)), _stream(a)), pool.handle, "laswp")
+    fn = _capi.lib().mla_laswp if check else _capi.lib().mla_laswp_async   # async: no host sync
+    _capi.check(fn(pool.handle, a.data_ptr(), rows, cols, ld, ip.data_ptr(), npiv,
+                   int(bool(reverse)), _stream(a)), pool.handle, "laswp")

@@ -137,7 +137,7 @@ def test_et_fires_and_ws_joins(mla):  # acceptance 4/5: ET cuts happen; panel SM
     assert r.et_events > 0
     d = mla.alloc_matrix(12288, 12288)
     mla.fill_random(d, 0, 2.0, -1.0)
-    r = mla.lu_la(d, mla.Policy("lu_mb", mla.BlockConfig(256, 32)))
+    r = mla.lu_la(d, mla.Policy("lu_mb", mla.BlockConfig(256, 32), t_pf=48))
     assert r.ws_joins > 0 and r.et_events == 0
 
 
@@ -194,3 +194,20 @@ def test_full_config3_rowscaled(mla):
 @pytest.mark.parametrize("b", [128, 256, 512, 768])
 def test_full_config4_block_sweep(mla, b):
     _full_config(mla, "config4", "lu_et", b=b)
+
+
+def test_distributed_driver_single_rank_cuda(mla):
+    """The multi-GPU driver with its CUDA operator table, degenerate P=1 (one GPU in this run):
+    same pack/unpack/apply code path as under NCCL, minus the broadcast."""
+    from paper_1611_06365_b200.distributed import DistLU
+    from paper_1611_06365_b200.workloads import LuConfig
+    n, b_o, b_i = 1536, 256, 32
+    cfg = LuConfig("t", n, "uniform", 4, b_o, b_i)
+    dlu = DistLU(n, b_o, b_i, cfg, "cuda", rank=0, world=1)
+    dlu.generate()
+    a_host = mla.make_matrix("uniform", n, 4)
+    assert np.array_equal(dlu.local_to_numpy(), a_host)
+    ipiv = dlu.factor()
+    ref = a_host.copy(order="F")
+    ro = oracle.lu_la(ref, b_o, b_i)
+    assert_parity(dlu.local_to_numpy(), ipiv, ref, ro.ipiv, "DistLU P=1")
