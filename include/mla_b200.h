@@ -141,6 +141,11 @@ int mla_panel_profile(mla_handle h, uint64_t* out16, int reset);
  * [4] scheduled width << 32 | factored width.  Returns the number of rows copied. Synchronises. */
 int mla_getrf_trace(mla_handle h, uint64_t* out, int max_rows);
 
+/* Time accounting of one update-team CTA during the last mla_getrf_la call (ns): [0] in GEMM tiles,
+ * [1] tile count, [2] in PREP items, [3] PREP count, [4] in LEFT items, [5] iteration barriers +
+ * bookkeeping, [6] whole kernel. */
+int mla_getrf_debug(mla_handle h, uint64_t* out8);
+
 /* residual_lu (matrix.py:116-131) has no entry point of its own: the Python layer composes it from
  * mla_laswp (P*A) and mla_gemm (blocked L*U), see paper_1611_06365_b200/matrix.py. */
 

@@ -238,8 +238,8 @@ extern "C" int mla_trsm_llu(mla_handle h, const double* L, int64_t w, int64_t ld
 
 // ---- laswp -----------------------------------------------------------------------------------------
 __global__ void k_laswp_plan(const int* ipiv, int npiv, int64_t rows, int reverse, PivPlan* plan, unsigned* ctrl) {
-  __shared__ int top[kMaxPiv], lrow[kMaxPiv], lcur[kMaxPiv], pv[kMaxPiv];
-  bool ok = build_pivot_plan(ipiv, npiv, rows, reverse != 0, plan->ref(), top, lrow, lcur, pv);
+  __shared__ int top[kMaxPiv], pv[kMaxPiv], keys[2 * kMaxPiv], vals[2 * kMaxPiv];
+  bool ok = build_pivot_plan(ipiv, npiv, rows, reverse != 0, plan->ref(), top, keys, vals, 2 * kMaxPiv, pv);
   if (threadIdx.x == 0) ctrl[CW_ERR_INDEX] = ok ? 0u : 1u;
 }
 
@@ -492,4 +492,11 @@ extern "C" int mla_getrf_trace(mla_handle h, uint64_t* out, int max_rows) {
   int rows = max_rows < kTraceCap ? max_rows : kTraceCap;
   CK(h, cudaMemcpy(out, h->lu_state->trace, (size_t)rows * 5 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return rows;
+}
+
+extern "C" int mla_getrf_debug(mla_handle h, uint64_t* out8) {
+  if (!h || !out8) return MLA_E_INVALID;
+  CK(h, cudaDeviceSynchronize());
+  CK(h, cudaMemcpy(out8, h->lu_state->dbg, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return MLA_OK;
 }

@@ -38,6 +38,7 @@ namespace mla {
 constexpr int kWidthsCap = 8192;
 constexpr int kMaxStrips = 1024;   // n <= 128 * 1024 columns
 constexpr int LEFT_CW = 256;       // columns per LEFT item
+constexpr int PREP_LOOKAHEAD = 12; // a strip is prepared this many strips ahead of its GEMM tiles
 
 struct LuState {
   // iteration descriptor: written by CTA 0 between two grid barriers, read by everybody after
@@ -53,6 +54,10 @@ struct LuState {
   // device trace (globaltimer ns), one row per outer iteration (first kTraceCap): [0] iteration
   // start, [1] PQ complete (panel may start), [2] panel end, [3] RQ complete, [4] width<<32|k_new
   unsigned long long trace[1024][5];
+  // accumulators of the LAST CTA of the grid (an RU CTA), globaltimer ns: [0] in GEMM tiles, [1] tile
+  // count, [2] in PREP items, [3] PREP count, [4] in LEFT items, [5] waiting at the iteration
+  // barriers + bookkeeping, [6] whole kernel
+  unsigned long long dbg[8];
 };
 constexpr int kTraceCap = 1024;
 
@@ -76,9 +81,10 @@ struct IterShape {
   int nps, tmc;                      // panel strips, row tiles
   int pq_prep, pq_total;
   int rcols, nrs, rq_prep, rq_gemm, nleft, rq_total;
+  int la_strips, gs;                 // PREP lookahead (strips) and RQ group size
 };
 
-__device__ __forceinline__ IterShape iter_shape(const LuState* st, int m, int n) {
+__device__ __forceinline__ IterShape iter_shape(const LuState* st, int m, int n, int grid) {
   IterShape s;
   s.q0 = *((volatile const int*)&st->q0);
   s.q1 = *((volatile const int*)&st->q1);
@@ -91,15 +97,21 @@ __device__ __forceinline__ IterShape iter_shape(const LuState* st, int m, int n)
   s.nps = (s.w + TRSM_CW - 1) / TRSM_CW;
   s.rcols = n - s.q1 - s.w;
   s.nrs = (s.rcols + TRSM_CW - 1) / TRSM_CW;
-  // PQ: [panel PREP][remainder PREP][panel GEMM] -- the remainder's PREP strips depend on nothing
-  // and fill the time the panel GEMM tiles would otherwise spend waiting for the panel PREP.
-  s.pq_prep = s.nps + s.nrs;
+  // PQ: [panel PREP][first PREP_LOOKAHEAD remainder PREPs][panel GEMM] -- those PREP strips depend
+  // on nothing and fill the time the panel GEMM tiles would otherwise wait for the panel PREP.
+  // enough fillers that every CTA of the grid has a PREP to do while the panel PREP runs
+  s.la_strips = imin(imax(PREP_LOOKAHEAD, grid - s.nps), s.nrs);
+  s.pq_prep = s.nps + s.la_strips;
   s.pq_total = s.pq_prep + s.nps * s.tmc;
-  // RQ: [remainder GEMM][LEFT]
+  // RQ: nrs groups of gs = tmc + 2 items: [PREP of strip s+lookahead][LEFT strip s][GEMM tiles of
+  // strip s]; then the LEFT strips that did not fit a group.  PREP and LEFT are HBM-bound row
+  // interchanges (+ a small trsm): spread between the tensor-bound GEMM tiles they overlap with them
+  // instead of saturating the memory system all at once at the start of the iteration.
   s.rq_prep = 0;
+  s.gs = s.tmc + 2;
   s.rq_gemm = s.nrs * s.tmc;
   s.nleft = (s.q0 + LEFT_CW - 1) / LEFT_CW;
-  s.rq_total = s.rq_gemm + s.nleft;
+  s.rq_total = s.nrs * s.gs + imax(0, s.nleft - s.nrs);
   return s;
 }
 
@@ -171,6 +183,45 @@ __device__ inline bool flag_ready(const unsigned* flag, unsigned v) {
 // (remainder + LEFT strips).  GEMM tiles run through the pipelined tile engine with a one-item
 // lookahead: while a tile finishes, the first k-slices of the next GEMM item (if its strip is already
 // prepared) are prefetched.  Returns the number of items executed, or -1 on abort.
+// Debug accumulators of one CTA live in shared memory during the run (a global read-modify-write per
+// tile would itself stall the tile pipeline) and are flushed to LuState::dbg at kernel end.
+__shared__ unsigned long long g_dbg[8];
+
+// One decoded queue item.
+struct QItem {
+  int kind;      // 0 no-op, 1 PREP of a panel strip, 2 PREP of a remainder strip, 3 GEMM tile, 4 LEFT strip
+  int strip;     // strip index (PREP/GEMM) or LEFT index
+  int tm;        // row tile (GEMM)
+};
+
+__device__ __forceinline__ QItem decode_item(const IterShape& s, int which, int t) {
+  QItem q{0, 0, 0};
+  if (which == 0) {
+    if (t < s.nps) { q.kind = 1; q.strip = t; }
+    else if (t < s.pq_prep) { q.kind = 2; q.strip = t - s.nps; }
+    else { int g = t - s.pq_prep; q.kind = 3; q.strip = g / s.tmc; q.tm = g - q.strip * s.tmc; }
+    return q;
+  }
+  const int ngrp = s.nrs * s.gs;
+  if (t < ngrp) {
+    const int grp = t / s.gs, slot = t - grp * s.gs;
+    if (slot == 0) {
+      int ps = grp + s.la_strips;
+      if (ps < s.nrs) { q.kind = 2; q.strip = ps; }
+    } else if (slot == 1) {
+      if (grp < s.nleft) { q.kind = 4; q.strip = grp; }
+    } else { q.kind = 3; q.strip = grp; q.tm = slot - 2; }
+    return q;
+  }
+  q.kind = 4;
+  q.strip = s.nrs + (t - ngrp);
+  return q;
+}
+
+// Drain one of the two queues of the iteration.  which == 0: PQ (next panel's columns), 1: RQ
+// (remainder + LEFT strips).  GEMM tiles run through the pipelined tile engine with a one-item
+// lookahead: while a tile finishes, the first k-slices of the next GEMM item (if its strip is already
+// prepared) are prefetched.  Returns the number of items executed, or -1 on abort.
 __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* smem, int which,
                                 bool signal_ru_done) {
   LuState* st = a.st;
@@ -178,72 +229,107 @@ __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* 
   unsigned* done = which ? &st->rq_done : &st->pq_done;
   unsigned* flags = which ? st->rprep_done : st->pprep_done;   // flags the GEMM tiles of this queue wait on
   const int total = which ? s.rq_total : s.pq_total;
-  const int nprep = which ? 0 : s.pq_prep;
   const int ngemm = which ? s.rq_gemm : s.nps * s.tmc;
   const int col_base = which ? (s.q1 + s.w) : s.q1;
   const int col_end = which ? a.n : (s.q1 + s.w);
   int executed = 0, base = 0;
   bool primed = false;
+  // Long queues (>= 16 tiles per CTA) pop one item further ahead with an atomic whose round trip
+  // overlaps the running tile's main loop; short queues keep the shallow lookahead so the last
+  // tiles of the iteration are not hoarded by one CTA.
+  const bool deep = ngemm >= 16 * (int)gridDim.x;
+  int ready_strip = -1;          // last strip whose PREP flag this CTA has seen set
+  unsigned long long dbg_last_end = 0ull;
+  __shared__ int s_fut;
   int t = pop_item(next);
+  int tn = 0;
+  bool have_tn = false;
   while (t < total) {
-    int tn;
-    if (t >= nprep && t < nprep + ngemm) {
-      const int g = t - nprep;
-      const int strip = g / s.tmc, tm = g - strip * s.tmc;
+    const QItem it = decode_item(s, which, t);
+    if (it.kind == 3) {
+      const int strip = it.strip;
       const int c0 = col_base + strip * TRSM_CW;
-      TileDesc cur = item_gemm_desc(a, s, tm, c0, imin(TRSM_CW, col_end - c0));
+      TileDesc cur = item_gemm_desc(a, s, it.tm, c0, imin(TRSM_CW, col_end - c0));
       if (!primed) {
-        if (!wait_flag_eq(&flags[strip], (unsigned)s.it, a.ctrl)) return -1;
+        if (strip != ready_strip && !wait_flag_eq(&flags[strip], (unsigned)s.it, a.ctrl)) return -1;
+        ready_strip = strip;
         base = 0;
         tile_prologue<GemmUpdateCfg>(cur, base, smem);
       }
-      tn = pop_item(next);
+      // no lookahead over the last G items of the queue: hoarding them would leave other CTAs idle
+      const bool look = t + (int)gridDim.x < total;
+      if (!have_tn && look) { tn = pop_item(next); have_tn = true; }
       TileDesc nxt{};
       nxt.valid = false;
       // chaining needs the current tile to span the whole prefetch window (KT >= STAGES-1): its
       // prologue was issued without knowing the successor
-      if (tn < nprep + ngemm && tn >= nprep && tile_kt<GemmUpdateCfg>(cur) >= GemmUpdateCfg::STAGES - 1) {
-        const int g2 = tn - nprep;
-        const int strip2 = g2 / s.tmc, tm2 = g2 - strip2 * s.tmc;
-        if (strip2 == strip || flag_ready(&flags[strip2], (unsigned)s.it)) {
-          const int c2 = col_base + strip2 * TRSM_CW;
-          nxt = item_gemm_desc(a, s, tm2, c2, imin(TRSM_CW, col_end - c2));
+      if (have_tn && tn < total && tile_kt<GemmUpdateCfg>(cur) >= GemmUpdateCfg::STAGES - 1) {
+        const QItem itn = decode_item(s, which, tn);
+        if (itn.kind == 3 && (itn.strip == ready_strip || flag_ready(&flags[itn.strip], (unsigned)s.it))) {
+          ready_strip = itn.strip;
+          const int c2 = col_base + itn.strip * TRSM_CW;
+          nxt = item_gemm_desc(a, s, itn.tm, c2, imin(TRSM_CW, col_end - c2));
         }
       }
+      unsigned fut = 0;
+      const bool fut_issued = deep && have_tn && tn + 2 * (int)gridDim.x < total;
+      if (fut_issued && threadIdx.x == 0)
+        asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(fut) : "l"(next) : "memory");
+      const bool dbgc = (blockIdx.x == gridDim.x - 1) && threadIdx.x == 0;
+      unsigned long long dt0 = dbgc ? globaltimer_ns() : 0ull;
+      if (dbgc && primed && dbg_last_end) g_dbg[7] += dt0 - dbg_last_end;   // gap between chained tiles
       base = tile_run<GemmUpdateCfg>(cur, nxt, base, smem);
+      if (dbgc) { unsigned long long now = globaltimer_ns(); g_dbg[0] += now - dt0; g_dbg[1] += 1; dbg_last_end = now; }
       primed = nxt.valid;
-    } else {
-      if (t < nprep) {
-        // PQ only: panel strips first, then the remainder's strips
-        if (t < s.nps) {
-          const int c0 = s.q1 + t * TRSM_CW;
-          item_prep(a, s, c0, imin(TRSM_CW, s.q1 + s.w - c0), &st->pprep_done[t], smem);
-        } else {
-          const int r = t - s.nps;
-          const int c0 = s.q1 + s.w + r * TRSM_CW;
-          item_prep(a, s, c0, imin(TRSM_CW, a.n - c0), &st->rprep_done[r], smem);
+      ++executed;
+      if (have_tn) {
+        t = tn;
+        have_tn = false;
+        if (fut_issued) {
+          if (threadIdx.x == 0) s_fut = (int)fut;
+          __syncthreads();
+          tn = s_fut;
+          have_tn = true;
+          __syncthreads();
         }
       } else {
-        const int l = t - nprep - ngemm;
-        const int c0 = l * LEFT_CW;
-        laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), a.plan->ref(), smem,
-                         kPlanCap * 4);
+        t = pop_item(next);
       }
-      primed = false;
-      tn = pop_item(next);
+      continue;
     }
+    const bool dbgc2 = (blockIdx.x == gridDim.x - 1) && threadIdx.x == 0;
+    unsigned long long dt1 = dbgc2 ? globaltimer_ns() : 0ull;
+    if (it.kind == 1) {
+      const int c0 = s.q1 + it.strip * TRSM_CW;
+      item_prep(a, s, c0, imin(TRSM_CW, s.q1 + s.w - c0), &st->pprep_done[it.strip], smem);
+    } else if (it.kind == 2) {
+      const int c0 = s.q1 + s.w + it.strip * TRSM_CW;
+      item_prep(a, s, c0, imin(TRSM_CW, a.n - c0), &st->rprep_done[it.strip], smem);
+    } else if (it.kind == 4) {
+      const int c0 = it.strip * LEFT_CW;
+      laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), a.plan->ref(), smem,
+                       kPlanCap * 4);
+    }
+    if (dbgc2 && it.kind != 0) {
+      if (it.kind <= 2) { g_dbg[2] += globaltimer_ns() - dt1; g_dbg[3] += 1; }
+      else g_dbg[4] += globaltimer_ns() - dt1;
+    }
+    primed = false;
     ++executed;
-    // completion; in RQ the CTA that finishes the last item announces RU done (lu.py:309-310)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      unsigned old = atom_add_release(done, 1u);
-      if (which && old + 1u == (unsigned)total) {
-        if (signal_ru_done) st_release(&st->ru_done, (unsigned)s.it);
-        if (s.it <= kTraceCap) st->trace[s.it - 1][3] = globaltimer_ns();
-      }
+    if (have_tn) { t = tn; have_tn = false; }
+    else t = pop_item(next);
+  }
+  // Completion is reported once per CTA, when it finds the queue empty: a per-item fence + atomic
+  // would stall the tile pipeline for two L2 round trips per tile.  The CTA whose report completes
+  // the count announces RU done (lu.py:309-310).
+  __syncthreads();
+  if (threadIdx.x == 0 && executed > 0) {
+    __threadfence();
+    unsigned old = atom_add_release(done, (unsigned)executed);
+    if (which && old + (unsigned)executed == (unsigned)total) {
+      if (signal_ru_done) st_release(&st->ru_done, (unsigned)s.it);
+      if (s.it <= kTraceCap) st->trace[s.it - 1][3] = globaltimer_ns();
     }
-    t = tn;
   }
   return executed;
 }
@@ -281,9 +367,14 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
   int singular = pr.singular, et_events = 0, n_panels = 0, ws_joins = 0;
   int q0 = 0, q1 = 0;
 
+  const bool dbgk = (bid == G - 1) && tid == 0;
+  if (tid < 8) g_dbg[tid] = 0ull;
+  __syncthreads();
+  const unsigned long long k_t0 = dbgk ? globaltimer_ns() : 0ull;
   while (true) {
     if (!all.ok) break;
     // ---- bookkeeping (lu.py:314-326) by CTA 0, between two grid barriers ----------------------------
+    unsigned long long b_t0 = dbgk ? globaltimer_ns() : 0ull;
     all.barrier();
     if (!all.ok) break;
     if (bid == 0) {
@@ -291,7 +382,7 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
       if (tid < 32) {
         int* scratch = reinterpret_cast<int*>(smem);
         build_pivot_plan(a.piv_local, k_new, (int64_t)(m - q1_of_panel), false, a.plan->ref(), scratch,
-                         scratch + kMaxPiv, scratch + 2 * kMaxPiv, scratch + 3 * kMaxPiv);
+                         scratch + kMaxPiv, scratch + 3 * kMaxPiv, 2 * kMaxPiv, scratch + 5 * kMaxPiv);
       }
       if (tid == 0) {
         if (a.widths && n_panels < a.widths_cap) a.widths[n_panels] = k_new;
@@ -312,8 +403,9 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
       }
     }
     all.barrier();
+    if (dbgk) g_dbg[5] += globaltimer_ns() - b_t0;
     if (!all.ok) break;
-    IterShape s = iter_shape(st, m, n);
+    IterShape s = iter_shape(st, m, n, G);
     if (*((volatile const int*)&st->done)) {
       // ---- final_sync (lu.py:328-332): last panel's interchanges for the columns to its left ------
       for (int l = bid; l < s.nleft; l += G) {
@@ -357,15 +449,15 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
         }
         if (ws && pf.ok) {
           // worker sharing: the quiesced panel team joins the update queue (pool.py:377-414)
-          if (a.variant == MLA_VARIANT_LU_WS_STATIC && s.rq_gemm > 0) {
+          if (a.variant == MLA_VARIANT_LU_WS_STATIC && s.rq_total > 0) {
             // join only at the next q-chunk boundary of the GEMM item range (lu.py:290-304)
             if (tid == 0) {
               int q = imax(1, a.q_chunks);
               unsigned head = ld_acquire(&st->rq_next);
-              int per = (s.rq_gemm + q - 1) / q;
-              int gpos = imax(0, (int)head - s.rq_prep);
+              int per = (s.rq_total + q - 1) / q;
+              int gpos = imax(0, (int)head);
               int next_chunk = ((gpos + per - 1) / per) * per;
-              unsigned wait_for = (unsigned)(s.rq_prep + imin(next_chunk, s.rq_gemm));
+              unsigned wait_for = (unsigned)imin(next_chunk, s.rq_total);
               spin_until_ge(&st->rq_next, wait_for, abort_word);
             }
             __syncthreads();
@@ -381,6 +473,10 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
     k_new = pr.cols_factored;
     singular |= pr.singular;
     if (is_pf && !pf.ok) { if (tid == 0) atomicExch(abort_word, 0xDEAD4u); }
+  }
+  if (dbgk) {
+    g_dbg[6] += globaltimer_ns() - k_t0;
+    for (int i = 0; i < 8; ++i) st->dbg[i] = g_dbg[i];
   }
   if (bid == 0 && tid == 0 && a.info) {
     a.info->cols_factored = n;

@@ -34,60 +34,58 @@ struct PivPlan {           // global-memory storage of one full-size plan
 };
 
 // Build the plan for ipiv[0..npiv) (view-local indices, view has `rows` rows).  Executed by ONE
-// warp (all 32 lanes call it); scratch: 4 arrays of npiv ints of shared memory (top/lrow/lcur/pv).
+// warp (all 32 lanes call it).  Shared scratch: top[npiv], pv[npiv], and an open-addressing hash
+// table keys[tsize]/vals[tsize] (tsize a power of two >= 2*npiv) that tracks the lower rows touched
+// so far.  The chain of npiv dependent swaps is simulated by lane 0 with O(1) shared-memory work per
+// step; validation and the final compaction are warp-parallel.
 // Returns false (and count = 0) if an index is out of range -- nothing may then be touched
 // (kernels.py:326-327).
 __device__ inline bool build_pivot_plan(const int* ipiv, int npiv, int64_t rows, bool reverse,
-                                        PlanRef plan, int* top, int* lrow, int* lcur, int* pv) {
+                                        PlanRef plan, int* top, int* keys, int* vals, int tsize, int* pv) {
   const int lane = threadIdx.x & 31;
   bool bad = false;
-  // the pivots are copied to shared scratch first: the simulation below is a chain of npiv
-  // dependent steps and must not pay a global-memory round trip per step
   for (int t = lane; t < npiv && t < kMaxPiv; t += 32) {
     int p = ipiv[t];
     if (p < 0 || (int64_t)p >= rows) bad = true;
     top[t] = t;
     pv[t] = p;
   }
+  for (int x = lane; x < tsize; x += 32) keys[x] = -1;
   bad = __any_sync(0xffffffffu, bad);
-  if (bad || npiv > kMaxPiv) {
+  if (bad || npiv > kMaxPiv || tsize < 2 * npiv) {
     if (lane == 0) *plan.count = 0;
     __syncwarp();
     return false;
   }
   __syncwarp();
-  int nlow = 0;  // entries in the lower list (uniform across lanes)
-  for (int s = 0; s < npiv; ++s) {
-    const int t = reverse ? (npiv - 1 - s) : s;
-    const int p = pv[t];
-    if (p == t) continue;
-    if (p < npiv) {
-      if (lane == 0) { int a = top[t]; top[t] = top[p]; top[p] = a; }
-      __syncwarp();
-    } else {
-      int found = -1;
-      for (int base = 0; base < nlow; base += 32) {
-        int e = base + lane;
-        unsigned m = __ballot_sync(0xffffffffu, e < nlow && lrow[e] == p);
-        if (m) { found = base + __ffs(m) - 1; break; }
+  if (lane == 0) {
+    const unsigned mask = (unsigned)tsize - 1u;
+    for (int s = 0; s < npiv; ++s) {
+      const int t = reverse ? (npiv - 1 - s) : s;
+      const int p = pv[t];
+      if (p == t) continue;
+      if (p < npiv) {
+        int a = top[t]; top[t] = top[p]; top[p] = a;
+      } else {
+        unsigned h = ((unsigned)p * 2654435761u) & mask;
+        while (true) {
+          int k = keys[h];
+          if (k == p) break;
+          if (k < 0) { keys[h] = p; vals[h] = p; break; }
+          h = (h + 1u) & mask;
+        }
+        int a = top[t]; top[t] = vals[h]; vals[h] = a;
       }
-      if (found < 0) {
-        found = nlow;
-        if (lane == 0) { lrow[nlow] = p; lcur[nlow] = p; }
-        ++nlow;
-        __syncwarp();
-      }
-      if (lane == 0) { int a = top[t]; top[t] = lcur[found]; lcur[found] = a; }
-      __syncwarp();
     }
   }
-  // compact the moves (identity moves dropped)
+  __syncwarp();
+  // compact the moves (identity moves dropped): top rows first, then the touched lower rows
   int cnt = 0;
-  for (int base = 0; base < npiv + nlow; base += 32) {
+  for (int base = 0; base < npiv + tsize; base += 32) {
     int e = base + lane;
     int d = -1, sidx = -1;
     if (e < npiv) { d = e; sidx = top[e]; }
-    else if (e < npiv + nlow) { d = lrow[e - npiv]; sidx = lcur[e - npiv]; }
+    else if (e < npiv + tsize && keys[e - npiv] >= 0) { d = keys[e - npiv]; sidx = vals[e - npiv]; }
     bool keep = (d >= 0) && (d != sidx);
     unsigned m = __ballot_sync(0xffffffffu, keep);
     if (keep) {
@@ -103,29 +101,58 @@ __device__ inline bool build_pivot_plan(const int* ipiv, int npiv, int64_t rows,
 }
 
 // Apply a plan to columns [0, ncols) of the view A (rows start at the plan's row 0).  Collective
-// over the CTA.  `buf` is shared memory holding at least cg*count doubles, cg >= 1 columns per
-// pass (buf_doubles gives its capacity).
+// over the CTA.  `buf` is shared memory of buf_doubles doubles; its tail holds a copy of the plan's
+// index lists, the rest stages CG columns per pass.  Each thread owns plan entries e = tid, tid+T, ..
+// and keeps LASWP_CG independent column loads in flight per entry (the moves are pure latency:
+// 8-byte accesses one sector each).
+constexpr int LASWP_CG = 8;
+
 __device__ inline void laswp_apply_cols(double* __restrict__ A, int64_t ld, int ncols, PlanRef plan,
                                         double* buf, int buf_doubles) {
   const int cnt = *plan.count;
   if (cnt <= 0 || ncols <= 0) return;
-  int cg = buf_doubles / cnt;
-  if (cg > 16) cg = 16;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // index lists at the end of the buffer (2*cnt ints = cnt doubles)
+  int* s_src = reinterpret_cast<int*>(buf + buf_doubles - cnt);
+  int* s_dst = s_src + cnt;
+  const int stage_cap = buf_doubles - cnt;
+  int cg = stage_cap / cnt;
+  if (cg > LASWP_CG) cg = LASWP_CG;
   if (cg < 1) return;  // cannot happen: callers size buf for kPlanCap
+  __syncthreads();
+  for (int e = tid; e < cnt; e += nt) { s_src[e] = plan.src[e]; s_dst[e] = plan.dst[e]; }
+  __syncthreads();
   for (int c0 = 0; c0 < ncols; c0 += cg) {
     const int nc = imin(cg, ncols - c0);
-    __syncthreads();
-    for (int x = threadIdx.x; x < nc * cnt; x += blockDim.x) {
-      int c = x / cnt, e = x - c * cnt;
-      buf[x] = A[(int64_t)(c0 + c) * ld + plan.src[e]];
+    double* __restrict__ base = A + (int64_t)c0 * ld;
+    if (nc == LASWP_CG) {
+      for (int e = tid; e < cnt; e += nt) {
+        const double* p = base + s_src[e];
+        double v[LASWP_CG];
+#pragma unroll
+        for (int c = 0; c < LASWP_CG; ++c) v[c] = p[(int64_t)c * ld];
+#pragma unroll
+        for (int c = 0; c < LASWP_CG; ++c) buf[c * cnt + e] = v[c];
+      }
+      __syncthreads();
+      for (int e = tid; e < cnt; e += nt) {
+        double* p = base + s_dst[e];
+#pragma unroll
+        for (int c = 0; c < LASWP_CG; ++c) p[(int64_t)c * ld] = buf[c * cnt + e];
+      }
+    } else {
+      for (int e = tid; e < cnt; e += nt) {
+        const double* p = base + s_src[e];
+        for (int c = 0; c < nc; ++c) buf[c * cnt + e] = p[(int64_t)c * ld];
+      }
+      __syncthreads();
+      for (int e = tid; e < cnt; e += nt) {
+        double* p = base + s_dst[e];
+        for (int c = 0; c < nc; ++c) p[(int64_t)c * ld] = buf[c * cnt + e];
+      }
     }
     __syncthreads();
-    for (int x = threadIdx.x; x < nc * cnt; x += blockDim.x) {
-      int c = x / cnt, e = x - c * cnt;
-      A[(int64_t)(c0 + c) * ld + plan.dst[e]] = buf[x];
-    }
   }
-  __syncthreads();
 }
 
 }  // namespace mla

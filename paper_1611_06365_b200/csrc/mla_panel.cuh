@@ -100,7 +100,7 @@ struct PanelShared {
   int plan_count;
   int plan_dst[2 * kMaxInner];
   int plan_src[2 * kMaxInner];
-  int plan_top[kMaxInner], plan_lrow[kMaxInner], plan_lcur[kMaxInner], plan_pv[kMaxInner];
+  int plan_top[kMaxInner], plan_pv[kMaxInner], plan_keys[2 * kMaxInner], plan_vals[2 * kMaxInner];
   int win_rank, win_row;
   double win_val;
   int flag;
@@ -287,21 +287,62 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       // flight together instead of forming a load->fma->store chain per column.
       const double pivot = sh.u[c];
       cv = -1.0; cr = 0x7fffffff;
-      for (int i = imax(r0, jc + 1) + tid; i < r1; i += kThreads) {
-        double* __restrict__ row = Sb + (i - r0);
-        const double l = row[(int64_t)c * lds] / pivot;
-        row[(int64_t)c * lds] = l;
-        for (int cb = c + 1; cb < wb; cb += 8) {
-          double x[8];
+      if (resident) {
+        for (int i = imax(r0, jc + 1) + tid; i < r1; i += kThreads) {
+          double* __restrict__ row = Sb + (i - r0);
+          const double l = row[(int64_t)c * lds] / pivot;
+          row[(int64_t)c * lds] = l;
+          for (int cb = c + 1; cb < wb; cb += 8) {
+            double x[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = (cb + e < wb) ? row[(int64_t)(cb + e) * lds] : 0.0;
+            for (int e = 0; e < 8; ++e) x[e] = (cb + e < wb) ? row[(int64_t)(cb + e) * lds] : 0.0;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) if (cb + e < wb) x[e] = fma(-l, sh.u[cb + e], x[e]);
+            for (int e = 0; e < 8; ++e) if (cb + e < wb) x[e] = fma(-l, sh.u[cb + e], x[e]);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) if (cb + e < wb) row[(int64_t)(cb + e) * lds] = x[e];
-          if (cb == c + 1) {
-            double v = fabs(x[0]);
-            if (cand_better(v, i, cv, cr)) { cv = v; cr = i; }
+            for (int e = 0; e < 8; ++e) if (cb + e < wb) row[(int64_t)(cb + e) * lds] = x[e];
+            if (cb == c + 1) {
+              double v = fabs(x[0]);
+              if (cand_better(v, i, cv, cr)) { cv = v; cr = i; }
+            }
+          }
+        }
+      } else {
+        // slab in global memory (too tall for shared memory): the pass is a stream through L2, so
+        // four rows per thread are kept in flight (32 independent 8-byte loads) to cover its latency
+        constexpr int RU = 4;
+        for (int ib = imax(r0, jc + 1) + tid; ib < r1; ib += kThreads * RU) {
+          double l[RU];
+          double* row[RU];
+#pragma unroll
+          for (int r = 0; r < RU; ++r) {
+            const int i = ib + r * kThreads;
+            row[r] = Sb + (imin(i, r1 - 1) - r0);
+            l[r] = row[r][(int64_t)c * lds];
+          }
+#pragma unroll
+          for (int r = 0; r < RU; ++r) {
+            l[r] = l[r] / pivot;
+            if (ib + r * kThreads < r1) row[r][(int64_t)c * lds] = l[r];
+          }
+          for (int cb = c + 1; cb < wb; cb += 8) {
+            double x[RU][8];
+#pragma unroll
+            for (int r = 0; r < RU; ++r)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) x[r][e] = (cb + e < wb) ? row[r][(int64_t)(cb + e) * lds] : 0.0;
+#pragma unroll
+            for (int r = 0; r < RU; ++r) {
+              const int i = ib + r * kThreads;
+              if (i < r1) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  if (cb + e < wb) row[r][(int64_t)(cb + e) * lds] = fma(-l[r], sh.u[cb + e], x[r][e]);
+                if (cb == c + 1) {
+                  double v = fabs(fma(-l[r], sh.u[cb], x[r][0]));
+                  if (cand_better(v, i, cv, cr)) { cv = v; cr = i; }
+                }
+              }
+            }
           }
         }
       }
@@ -324,8 +365,8 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
     if (w - wb > 0) {
       if (warp == 0) {
         PlanRef pr{&sh.plan_count, sh.plan_dst, sh.plan_src};
-        build_pivot_plan(sh.piv_rel, wb, (int64_t)(m - j), false, pr, sh.plan_top, sh.plan_lrow, sh.plan_lcur,
-                         sh.plan_pv);
+        build_pivot_plan(sh.piv_rel, wb, (int64_t)(m - j), false, pr, sh.plan_top, sh.plan_keys, sh.plan_vals,
+                         2 * kMaxInner, sh.plan_pv);
       }
       __syncthreads();
       PlanRef pr{&sh.plan_count, sh.plan_dst, sh.plan_src};

@@ -20,6 +20,9 @@ buf = (ctypes.c_uint64 * (5 * 1024))()
 got = _capi.lib().mla_getrf_trace(pool.handle, buf, 1024)
 t = np.array(buf[:5 * min(rows, got)], dtype=np.uint64).reshape(-1, 5).astype(np.int64)
 prof = (ctypes.c_uint64 * 16)(); _capi.lib().mla_panel_profile(pool.handle, prof, 1)
+dbg = (ctypes.c_uint64 * 8)(); _capi.lib().mla_getrf_debug(pool.handle, dbg)
+print("  RU CTA: gemm %.1f ms in %d tiles (%.2f us/tile), prep %.2f ms in %d (%.1f us each), left %.2f ms, barriers %.2f ms, kernel %.1f ms, chained-tile gaps %.2f ms" % (
+    dbg[0] / 1e6, dbg[1], dbg[0] / 1e3 / max(1, dbg[1]), dbg[2] / 1e6, dbg[3], dbg[2] / 1e3 / max(1, dbg[3]), dbg[4] / 1e6, dbg[5] / 1e6, dbg[6] / 1e6, dbg[7] / 1e6))
 print("  it   w  knew   pq_us panel_us   rq_us  iter_us   (pq: start->panel may start; panel: PF panel; rq: start->remainder done)")
 tot = {"pq": 0, "panel": 0, "rq": 0, "iter": 0}
 for i in range(len(t)):
