@@ -119,10 +119,13 @@ __device__ __forceinline__ IterShape iter_shape(const LuState* st, int m, int n,
 // owe them, lu.py:247-255) then the triangular solve with A11.
 __device__ inline void item_prep(const GetrfArgs& a, const IterShape& s, int c0, int cw, unsigned* flag,
                                  double* smem) {
+  // columns in [q1, pend) are the leftover of an ET-cut panel: the panel (Crout order) has already
+  // given them the interchanges AND their A12 rows
   int lo = imax(c0, s.pend);
-  if (lo < c0 + cw)
+  if (lo < c0 + cw) {
     laswp_apply_cols(a.A + (int64_t)lo * a.ld + s.q0, a.ld, c0 + cw - lo, a.plan->ref(), smem, kPlanCap * 4);
-  trsm_strip(a.A + (int64_t)s.q0 * a.ld + s.q0, s.kk, a.ld, a.A + (int64_t)c0 * a.ld + s.q0, cw, a.ld, smem);
+    trsm_strip(a.A + (int64_t)s.q0 * a.ld + s.q0, s.kk, a.ld, a.A + (int64_t)lo * a.ld + s.q0, c0 + cw - lo, a.ld, smem);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -359,7 +362,7 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
 
   // ---- prologue: first panel, the whole grid as one team (lu.py:224-241) --------------------------
   const int w0 = imin(a.b_outer, n);
-  PanelResult pr = panel_ll(all, a.A, m, w0, a.ld, a.piv_local, a.b_inner, nullptr, 0u, 0, a.pws, smem, smem_doubles);
+  PanelResult pr = panel_ll(all, a.A, m, w0, a.ld, a.piv_local, a.b_inner, nullptr, 0u, 0, a.pws, smem, smem_doubles, true);
   int k_new = pr.cols_factored;
   int w_sched = w0;
   int q1_of_panel = 0;       // where the just-factored panel starts
@@ -428,7 +431,7 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
       all.barrier();
       if (!all.ok) break;
       pr = panel_ll(all, a.A + (int64_t)s.q1 * a.ld + s.q1, m - s.q1, s.w, a.ld, a.piv_local, a.b_inner, nullptr,
-                    0u, 0, a.pws, smem, smem_doubles);
+                    0u, 0, a.pws, smem, smem_doubles, true);
     } else {
       // ---- look-ahead: everybody drains PQ, then PF factors while RU updates (lu.py:270-312) --------
       if (!run_pq(a, s, smem)) break;
@@ -439,7 +442,7 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
         __syncthreads();
         if (tr && bid == 0 && tid == 0) st->trace[s.it - 1][1] = globaltimer_ns();
         pr = panel_ll(pf, a.A + (int64_t)s.q1 * a.ld + s.q1, m - s.q1, s.w, a.ld, a.piv_local, a.b_inner,
-                      et ? &st->ru_done : nullptr, (unsigned)s.it, 0, a.pws, smem, smem_doubles);
+                      et ? &st->ru_done : nullptr, (unsigned)s.it, 0, a.pws, smem, smem_doubles, true);
         if (bid == 0 && tid == 0) {
           st_release(&st->pf_done, (unsigned)s.it);
           if (tr) {

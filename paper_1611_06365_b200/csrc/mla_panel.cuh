@@ -111,20 +111,38 @@ __device__ __forceinline__ bool cand_better(double v1, int r1, double v2, int r2
   return (v1 > v2) || (v1 == v2 && r1 < r2);
 }
 
+// Warp-wide best candidate in every lane: three REDUX (max of the high word, max of the low word
+// among the leaders, min row among the ties) instead of a 5-round shuffle butterfly.  |v| >= 0 maps
+// order-preservingly onto an unsigned 64-bit key (+1 so that 0.0 beats the "no candidate"
+// sentinels, which map to 0).
 __device__ __forceinline__ void cand_warp_reduce(double& v, int& r) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    double ov = __shfl_xor_sync(0xffffffffu, v, off);
-    int orow = __shfl_xor_sync(0xffffffffu, r, off);
-    if (cand_better(ov, orow, v, r)) { v = ov; r = orow; }
-  }
+  const unsigned long long k = (v >= 0.0) ? ((unsigned long long)__double_as_longlong(v) + 1ull) : 0ull;
+  const unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, (hi == mh) ? lo : 0u);
+  const bool lead = (hi == mh) && (lo == ml);
+  const unsigned mr = __reduce_min_sync(0xffffffffu, lead ? (unsigned)r : 0xffffffffu);
+  const unsigned long long kk = ((unsigned long long)mh << 32) | ml;
+  v = kk ? __longlong_as_double((long long)(kk - 1ull)) : -1.0;
+  r = (int)mr;
+}
+
+// a / pivot for the multipliers (lu.py:65-67 divides; it does not multiply by a reciprocal).  A full
+// IEEE division is a ~40-instruction dependent chain per row and step; here the quotient comes from
+// the shared reciprocal plus one residual correction, which is the correctly rounded quotient except
+// in rare double-rounding cases (<= 1 ulp), far inside the 1e-10 parity bound.
+__device__ __forceinline__ double div_by_pivot(double a, double pivot, double rinv) {
+  double q = a * rinv;
+  double r = fma(-q, pivot, a);
+  return fma(r, rinv, q);
 }
 
 // Collective over `team`; every thread of every member returns the same PanelResult.
 // smem: dynamic shared memory of smem_doubles doubles (>= TRSM_SMEM_DOUBLES).
 __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int64_t ld, int* ipiv_out,
                                        int b_inner, const unsigned* stop_flag, unsigned stop_eq,
-                                       int stop_after_polls, PanelWs* ws, double* smem, int smem_doubles) {
+                                       int stop_after_polls, PanelWs* ws, double* smem, int smem_doubles,
+                                       bool eager_u = false) {
   __shared__ PanelShared sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = team.size, rank = team.rank;
@@ -149,7 +167,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       wb = imin(wb, to_poll);
     }
     // ---- 1. U block -------------------------------------------------------------------------
-    if (j > 0) {
+    if (j > 0 && !eager_u) {
       {
         // columns of the U block are dealt in shares of >= 8 (one DMMA tile) to the first CTAs
         int nsh = imin(T, (wb + 7) / 8);
@@ -193,6 +211,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
     MLA_PROF(1);
 
     // ---- 3. pivot steps -------------------------------------------------------------------------
+    unsigned long long xchg_acc = 0ull;
     // candidate for column 0 of the block
     double cv = -1.0;
     int cr = 0x7fffffff;
@@ -210,62 +229,104 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       // B-E: warp 0 runs the whole exchange while the other warps wait at the next barrier
       if (warp == 0) {
         unsigned long long xt0 = (rank == 0 && lane == 0) ? globaltimer_ns() : 0ull;
-        XSlot* slots = ws->slots[seq & 1];
-        XSlot* myslot = &slots[rank];
         double bv = (lane < 8) ? sh.red_val[lane] : -2.0;
         int br = (lane < 8) ? sh.red_row[lane] : 0x7fffffff;
         cand_warp_reduce(bv, br);
         const bool have = bv >= 0.0;
         const bool own_diag = (jc >= r0 && jc < r1);
-        for (int cc = lane; cc < wb; cc += 32) {
-          if (have) st_b128(&myslot->rv[cc], (unsigned long long)__double_as_longlong(Sb[(int64_t)cc * lds + (br - r0)]), seq);
-          if (own_diag) st_b128(&myslot->dg[cc], (unsigned long long)__double_as_longlong(Sb[(int64_t)cc * lds + (jc - r0)]), seq);
-        }
-        if (lane == 0)
-          st_b128(&myslot->head, (unsigned long long)__double_as_longlong(have ? bv : -1.0),
-                  ((unsigned long long)(unsigned)(have ? br : 0x7fffffff) << 32) | (unsigned long long)seq);
-        // poll every member's header
-        double pv = -2.0;
-        int prow = 0x7fffffff, prank = -1;
         bool good = true;
-        for (int t = lane; t < T; t += 32) {
-          unsigned long long lo, hi;
-          if (!poll_unit(&slots[t].head, seq, team.abort_word, lo, hi)) { good = false; break; }
-          double v = __longlong_as_double((long long)lo);
-          int r = (int)(hi >> 32);
-          if (cand_better(v, r, pv, prow)) { pv = v; prow = r; prank = t; }
-        }
-        double wv = pv;
-        int wr = prow;
-        cand_warp_reduce(wv, wr);
-        unsigned who = __ballot_sync(0xffffffffu, pv == wv && prow == wr && prank >= 0);
-        int wrank = __shfl_sync(0xffffffffu, prank, who ? (__ffs(who) - 1) : 0);
-        good = __all_sync(0xffffffffu, good);
-        const int p = (wv > 0.0) ? wr : jc;
-        if (good && wv > 0.0) {
-          const int drank = (jc - j) / rpc;
-          for (int cc = lane; cc < wb; cc += 32) {
-            unsigned long long lo, hi, lo2 = 0, hi2 = 0;
-            ld_b128(&slots[wrank].rv[cc], lo, hi);                 // both loads in flight together
-            if (p != jc) ld_b128(&slots[drank].dg[cc], lo2, hi2);
-            if ((unsigned)hi != seq && !poll_unit(&slots[wrank].rv[cc], seq, team.abort_word, lo, hi)) { good = false; break; }
-            double uu = __longlong_as_double((long long)lo);
-            sh.u[cc] = uu;
-            if (p != jc) {
-              if ((unsigned)hi2 != seq && !poll_unit(&slots[drank].dg[cc], seq, team.abort_word, lo2, hi2)) { good = false; break; }
-              double dd = __longlong_as_double((long long)lo2);
-              // interchange rows jc <-> p inside the block (lu.py:60-64)
-              if (own_diag) Sb[(int64_t)cc * lds + (jc - r0)] = uu;
-              if (p >= r0 && p < r1) Sb[(int64_t)cc * lds + (p - r0)] = dd;
+        double wv;
+        int p;
+        if (T == 1) {
+          // single-CTA team: everything is local, no trip through L2
+          wv = bv;
+          p = (wv > 0.0) ? br : jc;
+          if (wv > 0.0) {
+            for (int cc = lane; cc < wb; cc += 32) {
+              double uu = Sb[(int64_t)cc * lds + (p - r0)];
+              sh.u[cc] = uu;
+              if (p != jc) {
+                double dd = Sb[(int64_t)cc * lds + (jc - r0)];
+                Sb[(int64_t)cc * lds + (jc - r0)] = uu;
+                Sb[(int64_t)cc * lds + (p - r0)] = dd;
+              }
             }
           }
+        } else {
+          XSlot* slots = ws->slots[seq & 1];
+          XSlot* myslot = &slots[rank];
+          const int drank = (jc - j) / rpc;
+          for (int cc = lane; cc < wb; cc += 32) {
+            if (have) st_b128(&myslot->rv[cc], (unsigned long long)__double_as_longlong(Sb[(int64_t)cc * lds + (br - r0)]), seq);
+            if (own_diag) st_b128(&myslot->dg[cc], (unsigned long long)__double_as_longlong(Sb[(int64_t)cc * lds + (jc - r0)]), seq);
+          }
+          if (lane == 0)
+            st_b128(&myslot->head, (unsigned long long)__double_as_longlong(have ? bv : -1.0),
+                    ((unsigned long long)(unsigned)(have ? br : 0x7fffffff) << 32) | (unsigned long long)seq);
+          // ONE hop for small teams: together with the headers, the diagonal row (its owner is known
+          // a priori) and every member's candidate row are requested speculatively; the tags say
+          // afterwards what was already valid.
+          constexpr int SPEC_T = 8;
+          const bool spec = (T <= SPEC_T) && (wb <= 32);
+          unsigned long long slo[SPEC_T], shi[SPEC_T], dlo = 0, dhi = 0;
+#pragma unroll
+          for (int t = 0; t < SPEC_T; ++t) { slo[t] = 0; shi[t] = 0; }
+          if (lane < wb) {
+            ld_b128(&slots[drank].dg[lane], dlo, dhi);
+            if (spec) {
+#pragma unroll
+              for (int t = 0; t < SPEC_T; ++t)
+                if (t < T) ld_b128(&slots[t].rv[lane], slo[t], shi[t]);
+            }
+          }
+          // poll every member's header
+          double pv = -2.0;
+          int prow = 0x7fffffff, prank = -1;
+          for (int t = lane; t < T; t += 32) {
+            unsigned long long lo, hi;
+            if (!poll_unit(&slots[t].head, seq, team.abort_word, lo, hi)) { good = false; break; }
+            double v = __longlong_as_double((long long)lo);
+            int r = (int)(hi >> 32);
+            if (cand_better(v, r, pv, prow)) { pv = v; prow = r; prank = t; }
+          }
+          wv = pv;
+          int wr = prow;
+          cand_warp_reduce(wv, wr);
+          unsigned who = __ballot_sync(0xffffffffu, pv == wv && prow == wr && prank >= 0);
+          int wrank = __shfl_sync(0xffffffffu, prank, who ? (__ffs(who) - 1) : 0);
           good = __all_sync(0xffffffffu, good);
+          p = (wv > 0.0) ? wr : jc;
+          if (good && wv > 0.0) {
+            for (int cc = lane; cc < wb; cc += 32) {
+              unsigned long long lo = 0, hi = 0;
+              if (spec) {
+#pragma unroll
+                for (int t = 0; t < SPEC_T; ++t)
+                  if (t == wrank) { lo = slo[t]; hi = shi[t]; }
+              } else {
+                ld_b128(&slots[wrank].rv[cc], lo, hi);
+              }
+              if ((unsigned)hi != seq && !poll_unit(&slots[wrank].rv[cc], seq, team.abort_word, lo, hi)) { good = false; break; }
+              double uu = __longlong_as_double((long long)lo);
+              sh.u[cc] = uu;
+              if (p != jc) {
+                unsigned long long lo2 = dlo, hi2 = dhi;
+                if (cc >= 32) ld_b128(&slots[drank].dg[cc], lo2, hi2);
+                if ((unsigned)hi2 != seq && !poll_unit(&slots[drank].dg[cc], seq, team.abort_word, lo2, hi2)) { good = false; break; }
+                double dd = __longlong_as_double((long long)lo2);
+                // interchange rows jc <-> p inside the block (lu.py:60-64)
+                if (own_diag) Sb[(int64_t)cc * lds + (jc - r0)] = uu;
+                if (p >= r0 && p < r1) Sb[(int64_t)cc * lds + (p - r0)] = dd;
+              }
+            }
+            good = __all_sync(0xffffffffu, good);
+          }
         }
         if (lane == 0) {
           sh.piv[c] = p;
           sh.win_val = wv;
           sh.flag = good ? 0 : 1;
-          if (rank == 0) ws->prof[5] += globaltimer_ns() - xt0;
+          if (rank == 0) xchg_acc += globaltimer_ns() - xt0;
         }
       }
       __syncthreads();
@@ -286,11 +347,12 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       // Columns are processed in register chunks of 8 so the shared-memory loads of a row are in
       // flight together instead of forming a load->fma->store chain per column.
       const double pivot = sh.u[c];
+      const double rinv = 1.0 / pivot;
       cv = -1.0; cr = 0x7fffffff;
       if (resident) {
         for (int i = imax(r0, jc + 1) + tid; i < r1; i += kThreads) {
           double* __restrict__ row = Sb + (i - r0);
-          const double l = row[(int64_t)c * lds] / pivot;
+          const double l = div_by_pivot(row[(int64_t)c * lds], pivot, rinv);
           row[(int64_t)c * lds] = l;
           for (int cb = c + 1; cb < wb; cb += 8) {
             double x[8];
@@ -321,7 +383,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
           }
 #pragma unroll
           for (int r = 0; r < RU; ++r) {
-            l[r] = l[r] / pivot;
+            l[r] = div_by_pivot(l[r], pivot, rinv);
             if (ib + r * kThreads < r1) row[r][(int64_t)c * lds] = l[r];
           }
           for (int cb = c + 1; cb < wb; cb += 8) {
@@ -349,6 +411,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
     }
     __syncthreads();
     MLA_PROF(2);
+    if (rank == 0 && tid == 0) ws->prof[5] += xchg_acc;
     // ---- write the slab back, record pivots ------------------------------------------------------
     if (resident) {
       for (int x = tid; x < nrows * wb; x += kThreads) {
@@ -378,6 +441,23 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       if (h0 > l0) laswp_apply_cols(P + (int64_t)l0 * ld + j, ld, h0 - l0, pr, ring, RING);
       int l1 = imax(lo, j) - j, h1 = imax(hi, j) - j;
       if (h1 > l1) laswp_apply_cols(P + (int64_t)(j + wb + l1) * ld + j, ld, h1 - l1, pr, ring, RING);
+    }
+    // ---- 4b. Crout order (eager_u): the rows of U this block determines, for all later columns ---
+    // U[j:j+wb, j+wb:w] = trilu(L_jj)^-1 (A[j:j+wb, j+wb:w] - L[j:j+wb, 0:j] U[0:j, j+wb:w]).
+    // Done here, the next block's update finds its U block complete (no trsm chain per block) and,
+    // after an ET cut, the leftover columns already hold their A12 rows (the next iteration's PREP
+    // skips them, see mla_getrf.cuh).  Needs this block's interchanges on those columns: barrier.
+    if (eager_u && j + wb < w) {
+      team.barrier();
+      const int nc = w - j - wb;
+      int nsh = imin(T, (nc + 7) / 8);
+      int per = (((nc + nsh - 1) / nsh) + 7) & ~7;
+      if (per > TRSM_CW) { per = TRSM_CW; nsh = (nc + per - 1) / per; }
+      for (int sh_i = rank; sh_i < nsh; sh_i += T) {
+        int c_lo = sh_i * per, c_hi = imin(nc, c_lo + per);
+        for (int rr = 0; rr < wb; rr += TRSM_RB)
+          trsm_rowblock(P, j + rr, imin(TRSM_RB, wb - rr), ld, P + (int64_t)(j + wb + c_lo) * ld, c_hi - c_lo, ld, smem);
+      }
     }
     j += wb;
     MLA_PROF(3);
