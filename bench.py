@@ -99,6 +99,49 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def phase_split(pool, res, n, b_o, flops):
+    """Update-vs-panel split of the LAST factorization from the device trace (mla_getrf_trace) and the
+    sampled update-team CTA (mla_getrf_debug): what BASELINE.json's config 4 asks for."""
+    import ctypes
+    from paper_1611_06365_b200 import _capi
+    lib = _capi.lib()
+    rows = max(0, len(res.widths) - 1)
+    buf = (ctypes.c_uint64 * (5 * 1024))()
+    got = lib.mla_getrf_trace(pool.handle, buf, 1024)
+    t = np.array(buf[:5 * min(rows, got)], dtype=np.uint64).reshape(-1, 5).astype(np.int64)
+    dbg = (ctypes.c_uint64 * 8)()
+    lib.mla_getrf_debug(pool.handle, dbg)
+    prof = (ctypes.c_uint64 * 16)()
+    lib.mla_panel_profile(pool.handle, prof, 1)
+    out = {}
+    if len(t):
+        ok = t[:, 3] > 0
+        pq = (t[:, 1] - t[:, 0]).clip(min=0)
+        panel = (t[:, 2] - t[:, 1]).clip(min=0)
+        rq = np.where(ok, t[:, 3] - t[:, 0], 0).clip(min=0)
+        nxt = np.append(t[1:, 0], max(t[-1, 2], t[-1, 3]))
+        it = nxt - t[:, 0]
+        bound_panel = int(np.sum((t[:, 2] > t[:, 3]) & ok))
+        out.update({
+            "iterations_traced": int(len(t)),
+            "sum_iteration_ms": round(float(it.sum()) / 1e6, 2),
+            "sum_update_queue_ms": round(float(rq.sum()) / 1e6, 2),
+            "sum_panel_ms": round(float(panel.sum()) / 1e6, 2),
+            "sum_panel_columns_update_ms": round(float(pq.sum()) / 1e6, 2),
+            "iterations_panel_bound": bound_panel,
+        })
+    if dbg[6]:
+        tile_us = dbg[0] / 1e3 / max(1, dbg[1])
+        out["update_cta_sample"] = {
+            "gemm_ms": round(dbg[0] / 1e6, 2), "tiles": int(dbg[1]), "us_per_tile": round(tile_us, 2),
+            "prep_ms": round(dbg[2] / 1e6, 2), "left_swaps_ms": round(dbg[4] / 1e6, 2),
+            "barrier_wait_ms": round(dbg[5] / 1e6, 2), "kernel_ms": round(dbg[6] / 1e6, 2)}
+    out["panel_team_rank0_ms"] = {"gemm": round(prof[1] / 1e6, 2), "pivot_steps": round(prof[2] / 1e6, 2),
+                                  "of_which_exchange": round(prof[5] / 1e6, 2),
+                                  "swaps_and_u_rows": round(prof[3] / 1e6, 2), "barriers": round(prof[4] / 1e6, 2)}
+    return out
+
+
 def pick(args, world):
     name = args.config or ("config4" if world == 1 else "config5")
     cfg = CONFIGS[name]
@@ -250,9 +293,13 @@ def run_ours(args):
     torch.cuda.synchronize()
     sampler.start()
     times = []
-    for _ in range(args.steps):
+    for step in range(args.steps):
         a.copy_(a0)            # restore (outside the timed region; also evicts L2: 8 GiB >> 126 MB)
         torch.cuda.synchronize()
+        if step == args.steps - 1:   # the phase split below describes the last step only
+            import ctypes
+            from paper_1611_06365_b200 import _capi
+            _capi.lib().mla_panel_profile(pool.handle, (ctypes.c_uint64 * 16)(), 1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         res = mla.lu_la(a, policy, pool)
@@ -263,6 +310,7 @@ def run_ours(args):
     ms = sum(times) / len(times)
     val = flops / (ms * 1e-3) / 1e9
 
+    phases = phase_split(pool, res, n, b_o, flops)
     residual = None
     if args.check:
         chk = mla.alloc_matrix(n, n, device=dev)
@@ -313,6 +361,7 @@ def run_ours(args):
                      "peak_source": "measured: DMMA.8x8x4 issue-bound rate, tools/fp64_peak.cu, "
                                     "profiles/r01_fp64_peak.log (MEASURED_PEAKS.json has no FP64 entry)"},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks,
+        "phases": phases,
     }
     if residual is not None:
         out["backward_error_over_n_eps"] = round(float(residual), 4)
