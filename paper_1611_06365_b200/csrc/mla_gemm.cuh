@@ -121,6 +121,46 @@ __device__ __forceinline__ void gemm_load_part_fast(double* smem, int slot, cons
   }
 }
 
+// Per-thread, per-tile constants of the fast path (hoisted out of the k loop).
+template <class Cfg>
+struct FastSrc {
+  const double* ap;     // A + ar*lda + ac            (+ kt*BK*lda per k-tile, + p*AROWS*lda per pass)
+  const double* bp;     // B + bc*ldb + bk            (+ kt*BK per k-tile,     + p*BCOLS*ldb per pass)
+  int kfull;            // number of whole BK slices (fast slices are kt < kfull); 0: tile not fast
+};
+
+template <class Cfg, class Desc>
+__device__ __forceinline__ FastSrc<Cfg> make_fast_src(const Desc& d) {
+  FastSrc<Cfg> f;
+  constexpr int ACH = Cfg::BM / 2, BCH = Cfg::BK / 2;
+  const int tid = threadIdx.x;
+  const bool fast = Cfg::FAST_OK && d.valid && ((((uintptr_t)d.A | (uintptr_t)d.B) & 15) == 0) &&
+                    ((d.lda & 1) == 0) && ((d.ldb & 1) == 0) && d.mrem >= Cfg::BM && d.nrem >= Cfg::BN;
+  f.kfull = fast ? d.K / Cfg::BK : 0;
+  f.ap = d.A + (int64_t)(tid / ACH) * d.lda + 2 * (tid % ACH);
+  f.bp = d.B + (int64_t)(tid / BCH) * d.ldb + 2 * (tid % BCH);
+  return f;
+}
+
+// Part `part` (of BK/4) of interior slice kt, all addresses from the hoisted constants.
+template <class Cfg>
+__device__ __forceinline__ void gemm_load_part_hoisted(double* sdstA, double* sdstB, int64_t a_pass, int64_t b_pass,
+                                                       const double* ap_kt, const double* bp_kt, int part) {
+  constexpr int PARTS = Cfg::BK / 4;
+  constexpr int ACH = Cfg::BM / 2, AROWS = kThreads / ACH, APASS = Cfg::BK / AROWS;
+  constexpr int BCH = Cfg::BK / 2, BCOLS = kThreads / BCH, BPASS = Cfg::BN / BCOLS;
+#pragma unroll
+  for (int pp = 0; pp < APASS / PARTS; ++pp) {
+    const int p = part * (APASS / PARTS) + pp;
+    cp_async16(sdstA + p * AROWS * Cfg::LDA_S, ap_kt + p * a_pass, 16);
+  }
+#pragma unroll
+  for (int pp = 0; pp < BPASS / PARTS; ++pp) {
+    const int p = part * (BPASS / PARTS) + pp;
+    cp_async16(sdstB + p * BCOLS * Cfg::LDB_S, bp_kt + p * b_pass, 16);
+  }
+}
+
 // Description of one C tile for the pipelined tile engine.
 struct TileDesc {
   const double* A; int64_t lda;       // mrem x K
@@ -196,15 +236,29 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
     }
   }
 
+  // fast-path constants of this tile and of the prefetched successor, hoisted out of the k loop
+  const FastSrc<Cfg> fd = make_fast_src<Cfg>(d);
+  FastSrc<Cfg> fn = make_fast_src<Cfg>(next);
+  if (next.valid && (next.lda != d.lda || next.ldb != d.ldb)) fn.kfull = 0;   // strides are shared below
+  constexpr int ACH_ = Cfg::BM / 2, BCH_ = Cfg::BK / 2;
+  const int64_t a_kt = (int64_t)Cfg::BK * d.lda;
+  const int64_t a_pass = (int64_t)(kThreads / ACH_) * d.lda, b_pass = (int64_t)(kThreads / BCH_) * d.ldb;
+  double* const sdA0 = smem + (tid / ACH_) * Cfg::LDA_S + 2 * (tid % ACH_);
+  double* const sdB0 = smem + Cfg::A_STAGE + (tid / BCH_) * Cfg::LDB_S + 2 * (tid % BCH_);
+
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int pos = kt + STAGES - 1;
     const int lslot = (base + pos) % STAGES;
-    const TileDesc& ld = (pos < KT) ? d : next;
-    const int lkt = (pos < KT) ? pos : pos - KT;
-    const bool lfast = tile_fast<Cfg>(ld, lkt);
-    if (!lfast) tile_issue<Cfg>(ld, lkt, lslot, smem);   // fringe / unaligned: whole slice at once
+    const bool cur_tile = pos < KT;
+    const int lkt = cur_tile ? pos : pos - KT;
+    const bool lfast = cur_tile ? (lkt < fd.kfull) : (lkt < fn.kfull);
+    const double* ap_kt = (cur_tile ? fd.ap : fn.ap) + lkt * a_kt;
+    const double* bp_kt = (cur_tile ? fd.bp : fn.bp) + lkt * Cfg::BK;
+    double* const sdA = sdA0 + lslot * Cfg::STAGE;
+    double* const sdB = sdB0 + lslot * Cfg::STAGE;
+    if (!lfast) tile_issue<Cfg>(cur_tile ? d : next, lkt, lslot, smem);   // fringe / unaligned: whole slice at once
     const double* sA = smem + ((base + kt) % STAGES) * Cfg::STAGE;
     const double* sB = sA + Cfg::A_STAGE;
     const double* pa = sA + q * Cfg::LDA_S + wi * Cfg::WTI + g;       // + k4*4*LDA_S + ni*8
@@ -217,7 +271,7 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
 #pragma unroll
       for (int a = 0; a < NJ; ++a) fj[a] = pb[a * 8 * Cfg::LDB_S + k4 * 4];
       if constexpr (Cfg::FAST_OK) {
-        if (lfast) gemm_load_part_fast<Cfg>(smem, lslot, ld.A, ld.lda, ld.B, ld.ldb, lkt, k4);
+        if (lfast) gemm_load_part_hoisted<Cfg>(sdA, sdB, a_pass, b_pass, ap_kt, bp_kt, k4);
       }
 #pragma unroll
       for (int a = 0; a < NJ; ++a)
