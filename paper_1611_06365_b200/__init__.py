@@ -13,13 +13,14 @@ from .matrix import (PivotVector, alloc_matrix, fill_random, frobenius_norm, fro
                      leading_dimension, partition_2x2, residual_lu, residual_packed, split_lu,
                      swap_rows, to_numpy)
 from .pool import CompletionFlag, SmPool, WorkerPool, default_pool, signal_complete
+from .trace import TraceEvent, check_trace, load_jsonl
 from .workloads import CONFIGS, LuConfig, flops_lu, make_config_matrix, make_matrix
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BlockConfig", "CacheConfig", "CompletionFlag", "CONFIGS", "CountingStop", "LuConfig", "LuResult",
-    "PivotVector", "Policy", "SmPool", "VARIANTS", "WorkerPool", "alloc_matrix", "default_pool",
+    "PivotVector", "Policy", "SmPool", "TraceEvent", "VARIANTS", "WorkerPool", "check_trace", "load_jsonl", "alloc_matrix", "default_pool",
     "et_schedule_from", "et_widths_from", "fill_random", "flops_lu", "frobenius_norm", "from_numpy",
     "gemm_malleable", "laswp", "leading_dimension", "lu_blk_ll", "lu_blk_rl", "lu_la", "lu_unb",
     "make_config_matrix", "make_matrix", "partition_2x2", "residual_lu", "residual_packed",

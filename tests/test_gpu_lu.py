@@ -211,3 +211,34 @@ def test_distributed_driver_single_rank_cuda(mla):
     ref = a_host.copy(order="F")
     ro = oracle.lu_la(ref, b_o, b_i)
     assert_parity(dlu.local_to_numpy(), ipiv, ref, ro.ipiv, "DistLU P=1")
+
+
+def test_device_trace_is_a_valid_reference_trace(mla, tmp_path):  # acceptance 4 (test_acceptance.py:192-218)
+    from paper_1611_06365_b200 import trace as mtrace
+    pool = mla.default_pool()
+    a = mla.alloc_matrix(12288, 12288)
+    mla.fill_random(a, 0, 2.0, -1.0)
+    r = mla.lu_la(a, mla.Policy("lu_mb", mla.BlockConfig(256, 32), t_pf=48), pool)
+    evs = mtrace.events_from_result(pool, r, "lu_mb", 48)
+    assert evs
+    mtrace.check_trace(evs)
+    path = str(tmp_path / "trace.jsonl")
+    mtrace.write_jsonl(evs, path)
+    assert mtrace.load_jsonl(path) == evs
+    merged = {e.iter_index for e in evs if e.team == "MERGED"}
+    assert merged and r.ws_joins > 0                 # panel SMs joined the update in some iterations
+    idle = mtrace.pf_idle_fraction(evs)
+    assert all(idle[it] < 0.10 for it in merged)     # with merging the panel worker has (almost) no idle gap
+
+
+def test_bench_cli_csv(mla, capsys):  # reference test_bench.py: header, seed reproducibility, --check gate
+    from paper_1611_06365_b200 import bench_cli
+    assert bench_cli.main(["--algo", "lu_et", "--n", "1024", "--b-outer", "128", "--b-inner", "32", "--check",
+                           "--seed", "5"]) == 0
+    out = capsys.readouterr().out.strip().splitlines()
+    assert out[0] == ",".join(bench_cli.CSV_FIELDS)
+    row = out[1].split(",")
+    assert row[0] == "lu_et" and row[1] == "1024" and float(row[9]) <= 1024 * 100 * EPS
+    assert bench_cli.main(["--gepp", "--n", "1024", "--sweep-b", "64:128:64"]) == 0
+    out = capsys.readouterr().out.strip().splitlines()
+    assert out[0] == "k,gflops" and len(out) == 3

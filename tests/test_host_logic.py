@@ -105,3 +105,34 @@ def test_config3_pivot_distance_is_reported_not_assumed():
     b = np.asfortranarray(make_matrix("normal", n, 2))
     dist_normal = float(np.mean(oracle.lu_la(b, 128, 16).ipiv - np.arange(n)))
     assert dist_scaled < dist_normal
+
+
+def test_bench_cli_argument_rules():  # reference test_bench.py: exit code 2 on bad arguments, CSV header
+    from paper_1611_06365_b200 import bench_cli
+    assert bench_cli.CSV_FIELDS == ("variant", "n", "b_outer", "b_inner", "threads", "t_pf", "seed",
+                                    "wall_seconds", "gflops", "residual", "et_events")
+    for argv in ([], ["--gepp"], ["--n", "64", "--b-outer", "8", "--b-inner", "16"],
+                 ["--n", "64", "--b-inner", "0"], ["--n", "64", "--algo", "nope"], ["--n", "64", "--sweep-b", "3:1:1"]):
+        with pytest.raises(SystemExit) as ei:
+            ap = bench_cli.build_parser()
+            bench_cli.validate(ap, ap.parse_args(argv))
+        assert ei.value.code == 2
+    ap = bench_cli.build_parser()
+    args = ap.parse_args(["--n", "128", "--algo", "lu_et", "--sweep-b", "32:96:32"])
+    bench_cli.validate(ap, args)
+    assert args.sweep_b == [32, 64, 96]
+
+
+def test_trace_rules_match_reference():  # reference trace.py:69-99 / test_trace.py
+    from paper_1611_06365_b200.trace import TraceEvent, check_trace, iteration_spans, pf_idle_fraction
+    ok = [TraceEvent(0, "PF", "GEMM", 0, 10, 1), TraceEvent(0, "PF", "PANEL", 10, 50, 1),
+          TraceEvent(0, "MERGED", "GEMM", 50, 80, 1), TraceEvent(16, "RU", "GEMM", 0, 80, 1)]
+    check_trace(ok)
+    assert iteration_spans(ok) == {1: (0, 80)}
+    assert abs(pf_idle_fraction(ok)[1]) < 1e-12
+    with pytest.raises(ValueError):   # merged before the panel ended
+        check_trace([TraceEvent(0, "PF", "PANEL", 10, 50, 1), TraceEvent(1, "MERGED", "GEMM", 40, 80, 1)])
+    with pytest.raises(ValueError):   # overlap on one worker
+        check_trace([TraceEvent(0, "PF", "GEMM", 0, 10, 1), TraceEvent(0, "PF", "PANEL", 5, 50, 1)])
+    with pytest.raises(ValueError):
+        check_trace([TraceEvent(0, "PF", "NOPE", 0, 1, 1)])
