@@ -84,43 +84,11 @@ __device__ __forceinline__ void gemm_load_stage(double* smem, int slot, const do
   }
 }
 
-// Fast path of gemm_load_stage: interior tile (mrem == BM, nrem == BN), whole BK slice inside K,
-// 16-byte aligned operands.  All address arithmetic is a per-thread base plus compile-time strides.
-// The slice is cut into PARTS = BK/4 parts so the main loop can issue one part per k4 step: a burst
-// of LDGSTS at the top of a k-tile would sit in the MIO queue in front of the fragment LDS.64 and
-// starve the DMMA pipe.
-template <class Cfg>
-__device__ __forceinline__ void gemm_load_part_fast(double* smem, int slot, const double* __restrict__ A,
-                                                    int64_t lda, const double* __restrict__ B, int64_t ldb,
-                                                    int kt, int part) {
-  double* sA = smem + slot * Cfg::STAGE;
-  double* sB = sA + Cfg::A_STAGE;
-  const int tid = threadIdx.x;
-  constexpr int PARTS = Cfg::BK / 4;
-  constexpr int ACH = Cfg::BM / 2;                 // 16-byte chunks per k-row of the A slice
-  constexpr int AROWS = kThreads / ACH;            // k-rows covered per pass
-  constexpr int APASS = Cfg::BK / AROWS;
-  const int ar = tid / ACH, ac = 2 * (tid % ACH);
-  const double* ap = A + (int64_t)(kt * Cfg::BK + ar) * lda + ac;
-  double* ad = sA + ar * Cfg::LDA_S + ac;
-#pragma unroll
-  for (int pp = 0; pp < APASS / PARTS; ++pp) {
-    const int p = part * (APASS / PARTS) + pp;
-    cp_async16(ad + p * AROWS * Cfg::LDA_S, ap + (int64_t)(p * AROWS) * lda, 16);
-  }
-  constexpr int BCH = Cfg::BK / 2;                 // chunks per column of the B slice
-  constexpr int BCOLS = kThreads / BCH;            // columns covered per pass
-  constexpr int BPASS = Cfg::BN / BCOLS;
-  const int bc = tid / BCH, bk = 2 * (tid % BCH);
-  const double* bp = B + (int64_t)bc * ldb + kt * Cfg::BK + bk;
-  double* bd = sB + bc * Cfg::LDB_S + bk;
-#pragma unroll
-  for (int pp = 0; pp < BPASS / PARTS; ++pp) {
-    const int p = part * (BPASS / PARTS) + pp;
-    cp_async16(bd + p * BCOLS * Cfg::LDB_S, bp + (int64_t)(p * BCOLS) * ldb, 16);
-  }
-}
-
+// Fast path of the staging: interior tile (mrem == BM, nrem == BN), whole BK slice inside K, 16-byte
+// aligned operands.  All address arithmetic is a per-thread base plus compile-time strides, hoisted out
+// of the k loop.  The slice is cut into PARTS = BK/4 parts so the main loop can issue one part per k4
+// step: a burst of LDGSTS at the top of a k-tile would sit in the MIO queue in front of the fragment
+// LDS.64 and starve the DMMA pipe.
 // Per-thread, per-tile constants of the fast path (hoisted out of the k loop).
 template <class Cfg>
 struct FastSrc {
@@ -174,14 +142,6 @@ struct TileDesc {
 
 template <class Cfg>
 __device__ __forceinline__ int tile_kt(const TileDesc& d) { return (d.K + Cfg::BK - 1) / Cfg::BK; }
-
-// Can k-tile kt of tile d take the unpredicated fast path?
-template <class Cfg>
-__device__ __forceinline__ bool tile_fast(const TileDesc& d, int kt) {
-  if (!Cfg::FAST_OK) return false;
-  return d.valid && ((((uintptr_t)d.A | (uintptr_t)d.B) & 15) == 0) && ((d.lda & 1) == 0) && ((d.ldb & 1) == 0) &&
-         d.mrem >= Cfg::BM && d.nrem >= Cfg::BN && (kt + 1) * Cfg::BK <= d.K;
-}
 
 // Issue (and commit as one group) the loads of k-tile `kt` of tile d into ring slot `slot`; an
 // out-of-range kt or an invalid tile commits an empty group so that group accounting stays uniform.
@@ -378,16 +338,6 @@ __device__ __forceinline__ TileDesc gemm_tile_desc(const GemmProblem& p, int t) 
   double* c = p.C + (int64_t)j0 * p.ldc + i0;
   return TileDesc{p.A + i0, p.lda, p.B + (int64_t)j0 * p.ldb, p.ldb, c, p.ldc, c, p.ldc,
                   p.k, p.m - i0, p.n - j0, p.alpha, p.beta, true};
-}
-
-template <class Cfg>
-__device__ __forceinline__ void gemm_run_tile(const GemmProblem& p, int t, double* smem) {
-  const int tm_count = (p.m + Cfg::BM - 1) / Cfg::BM;
-  const int tm = t % tm_count, tn = t / tm_count;
-  const int i0 = tm * Cfg::BM, j0 = tn * Cfg::BN;
-  double* c = p.C + (int64_t)j0 * p.ldc + i0;
-  gemm_tile<Cfg>(p.A + i0, p.lda, p.B + (int64_t)j0 * p.ldb, p.ldb, p.k, c, p.ldc, c, p.ldc,
-                 p.m - i0, p.n - j0, p.alpha, p.beta, smem);
 }
 
 }  // namespace mla
