@@ -251,7 +251,7 @@ k_laswp_apply(double* A, int64_t cols, int64_t ld, PivPlan* plan) {
   per = (per + 15) & ~(int64_t)15;
   int64_t lo = blockIdx.x * per, hi = lo + per < cols ? lo + per : cols;
   if (lo >= hi) return;
-  laswp_apply_cols(A + lo * ld, ld, (int)(hi - lo), plan->ref(), smem, kPlanCap * 4);
+  laswp_apply_cols(A + lo * ld, ld, (int)(hi - lo), plan->ref(), smem, kLaswpBufDoubles);
 }
 
 static int laswp_impl(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
@@ -272,7 +272,7 @@ static int laswp_impl(mla_handle h, double* A, int64_t rows, int64_t cols, int64
   if (!h || rows < 0 || cols < 0 || npiv < 0 || (rows > 0 && ld < rows)) return MLA_E_INVALID;
   if (npiv == 0) return MLA_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const int smem_bytes = kPlanCap * 4 * 8;
+  const int smem_bytes = kLaswpBufDoubles * 8;
   CK(h, cudaFuncSetAttribute(k_laswp_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
   // pivot blocks wider than one plan are applied as consecutive chunks (ascending for forward,
   // descending for reverse); chunk c works on the view that starts at its first row.

@@ -123,7 +123,7 @@ __device__ inline void item_prep(const GetrfArgs& a, const IterShape& s, int c0,
   // given them the interchanges AND their A12 rows
   int lo = imax(c0, s.pend);
   if (lo < c0 + cw) {
-    laswp_apply_cols(a.A + (int64_t)lo * a.ld + s.q0, a.ld, c0 + cw - lo, a.plan->ref(), smem, kPlanCap * 4);
+    laswp_apply_cols(a.A + (int64_t)lo * a.ld + s.q0, a.ld, c0 + cw - lo, a.plan->ref(), smem, kLaswpBufDoubles);
     trsm_strip(a.A + (int64_t)s.q0 * a.ld + s.q0, s.kk, a.ld, a.A + (int64_t)lo * a.ld + s.q0, c0 + cw - lo, a.ld, smem);
   }
   __syncthreads();
@@ -311,7 +311,7 @@ __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* 
     } else if (it.kind == 4) {
       const int c0 = it.strip * LEFT_CW;
       laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), a.plan->ref(), smem,
-                       kPlanCap * 4);
+                       kLaswpBufDoubles);
     }
     if (dbgc2 && it.kind != 0) {
       if (it.kind <= 2) { g_dbg[2] += globaltimer_ns() - dt1; g_dbg[3] += 1; }
@@ -414,7 +414,7 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
       for (int l = bid; l < s.nleft; l += G) {
         int c0 = l * LEFT_CW;
         laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), a.plan->ref(), smem,
-                         kPlanCap * 4);
+                         kLaswpBufDoubles);
       }
       break;
     }

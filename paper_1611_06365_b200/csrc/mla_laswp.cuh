@@ -105,7 +105,8 @@ __device__ inline bool build_pivot_plan(const int* ipiv, int npiv, int64_t rows,
 // index lists, the rest stages CG columns per pass.  Each thread owns plan entries e = tid, tid+T, ..
 // and keeps LASWP_CG independent column loads in flight per entry (the moves are pure latency:
 // 8-byte accesses one sector each).
-constexpr int LASWP_CG = 8;
+constexpr int LASWP_CG = 16;
+constexpr int kLaswpBufDoubles = 20 * 1024;   // staging buffer the callers provide (160 KiB)
 
 __device__ inline void laswp_apply_cols(double* __restrict__ A, int64_t ld, int ncols, PlanRef plan,
                                         double* buf, int buf_doubles) {
