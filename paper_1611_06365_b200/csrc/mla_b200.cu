@@ -175,6 +175,51 @@ k_gemm(GemmProblem p, unsigned* ctrl, const unsigned* join_flag, int donors) {
   }
 }
 
+// EXPERIMENT (tools/dev_gemm_half.py): the same tile engine as 128-thread CTAs on 128x64 tiles, two CTAs
+// per SM, so that one CTA's epilogue / barrier bubbles overlap the other's DMMA stream.
+__global__ void __launch_bounds__(128, 2)
+k_gemm_half(GemmProblem p, unsigned* ctrl) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_tile;
+  using Cfg = GemmHalfCfg;
+  const int ntiles = gemm_num_tiles<Cfg>(p);
+  auto pop = [&]() {
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(ctrl + CW_QUEUE_NEXT, 1u);
+    __syncthreads();
+    int t = s_tile;
+    __syncthreads();
+    return t;
+  };
+  int t = pop();
+  if (t >= ntiles) return;
+  TileDesc cur = gemm_tile_desc<Cfg>(p, t);
+  int base = 0;
+  tile_prologue<Cfg>(cur, base, smem);
+  while (true) {
+    int tn = pop();
+    TileDesc nxt{};
+    nxt.valid = false;
+    if (tn < ntiles && tile_kt<Cfg>(cur) >= Cfg::STAGES - 1) nxt = gemm_tile_desc<Cfg>(p, tn);
+    base = tile_run<Cfg>(cur, nxt, base, smem);
+    if (nxt.valid) { cur = nxt; continue; }
+    if (tn >= ntiles) break;
+    cur = gemm_tile_desc<Cfg>(p, tn);
+    base = 0;
+    tile_prologue<Cfg>(cur, base, smem);
+  }
+}
+
+extern "C" int mla_gemm_half_experiment(mla_handle h, double* C, int64_t m, int64_t n, int64_t ldc, const double* A,
+                                        int64_t lda, const double* B, int64_t ldb, int64_t k, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  GemmProblem p{C, ldc, A, lda, B, ldb, (int)m, (int)n, (int)k, 1.0, -1.0};
+  CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
+  CK(h, cudaFuncSetAttribute(k_gemm_half, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmHalfCfg::SMEM_BYTES));
+  k_gemm_half<<<2 * h->num_sms, 128, GemmHalfCfg::SMEM_BYTES, s>>>(p, h->ctrl);
+  CK(h, cudaGetLastError());
+  return MLA_OK;
+}
+
 __global__ void k_scale(double* C, int64_t m, int64_t n, int64_t ldc, double alpha) {
   for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)

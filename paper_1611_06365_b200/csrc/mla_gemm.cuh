@@ -19,10 +19,11 @@
 
 namespace mla {
 
-template <int BM_, int BN_, int WI_, int WJ_, int STAGES_, int BK_ = 16>
+template <int BM_, int BN_, int WI_, int WJ_, int STAGES_, int BK_ = 16, int THREADS_ = kThreads>
 struct GemmCfg {
   static constexpr int BM = BM_, BN = BN_, WI = WI_, WJ = WJ_, STAGES = STAGES_;
   static constexpr int BK = BK_;
+  static constexpr int THREADS = THREADS_;   // threads of the CTA (or thread group) running the tile
   static constexpr int LDA_S = BM + 4;  // (BM+4) % 16 == 4 -> conflict-free fragment loads
   static constexpr int LDB_S = BK + 4;
   static constexpr int A_STAGE = BK * LDA_S;
@@ -33,14 +34,15 @@ struct GemmCfg {
   static constexpr int NI = WTI / 8, NJ = WTJ / 8;
   // can the slice be issued as BK/4 equal unpredicated parts (one per k4 step)?
   static constexpr int PARTS = BK / 4;
-  static constexpr bool FAST_OK = (kThreads % (BM / 2) == 0) && (BK % (kThreads / (BM / 2)) == 0) &&
-                                  ((BK / (kThreads / (BM / 2))) % PARTS == 0) && (kThreads % (BK / 2) == 0) &&
-                                  (BN % (kThreads / (BK / 2)) == 0) && ((BN / (kThreads / (BK / 2))) % PARTS == 0);
-  static_assert(WI * WJ * 32 == kThreads, "8 warps");
+  static constexpr bool FAST_OK = (THREADS % (BM / 2) == 0) && (BK % (THREADS / (BM / 2)) == 0) &&
+                                  ((BK / (THREADS / (BM / 2))) % PARTS == 0) && (THREADS % (BK / 2) == 0) &&
+                                  (BN % (THREADS / (BK / 2)) == 0) && ((BN / (THREADS / (BK / 2))) % PARTS == 0);
+  static_assert(WI * WJ * 32 == THREADS, "one warp per (WI, WJ) cell");
   static_assert(BM % 16 == 0 && BN % 8 == 0 && WTI % 8 == 0 && WTJ % 8 == 0, "tile shape");
 };
 
 using GemmUpdateCfg = GemmCfg<128, 128, 2, 4, 3, 32>;  // trailing update tiles
+using GemmHalfCfg = GemmCfg<128, 64, 2, 2, 2, 32, 128>;   // experiment: 128-thread CTAs, two per SM
 using GemmPanelCfg = GemmCfg<128, 32, 8, 1, 4>;    // panel-internal update (N = inner block)
 using GemmTrsmCfg = GemmCfg<32, 128, 1, 8, 4>;     // row-block update inside trsm strips
 
@@ -55,27 +57,27 @@ __device__ __forceinline__ void gemm_load_stage(double* smem, int slot, const do
   const int tid = threadIdx.x;
   if (AL16) {
     constexpr int ACH = Cfg::BM / 2;
-    for (int c = tid; c < Cfg::BK * ACH; c += kThreads) {
+    for (int c = tid; c < Cfg::BK * ACH; c += Cfg::THREADS) {
       int kk = c / ACH, i = 2 * (c % ACH);
       int valid = (k0 + kk < K) ? imin(imax(mrem - i, 0), 2) * 8 : 0;
       const double* src = valid ? (A + (int64_t)(k0 + kk) * lda + i) : A;
       cp_async16(sA + kk * Cfg::LDA_S + i, src, valid);
     }
     constexpr int BCH = Cfg::BK / 2;
-    for (int c = tid; c < Cfg::BN * BCH; c += kThreads) {
+    for (int c = tid; c < Cfg::BN * BCH; c += Cfg::THREADS) {
       int j = c / BCH, kk = 2 * (c % BCH);
       int valid = (j < nrem) ? imin(imax(K - (k0 + kk), 0), 2) * 8 : 0;
       const double* src = valid ? (B + (int64_t)j * ldb + k0 + kk) : B;
       cp_async16(sB + j * Cfg::LDB_S + kk, src, valid);
     }
   } else {
-    for (int c = tid; c < Cfg::BK * Cfg::BM; c += kThreads) {
+    for (int c = tid; c < Cfg::BK * Cfg::BM; c += Cfg::THREADS) {
       int kk = c / Cfg::BM, i = c % Cfg::BM;
       int valid = (k0 + kk < K && i < mrem) ? 8 : 0;
       const double* src = valid ? (A + (int64_t)(k0 + kk) * lda + i) : A;
       cp_async8(sA + kk * Cfg::LDA_S + i, src, valid);
     }
-    for (int c = tid; c < Cfg::BN * Cfg::BK; c += kThreads) {
+    for (int c = tid; c < Cfg::BN * Cfg::BK; c += Cfg::THREADS) {
       int j = c / Cfg::BK, kk = c % Cfg::BK;
       int valid = (j < nrem && k0 + kk < K) ? 8 : 0;
       const double* src = valid ? (B + (int64_t)j * ldb + k0 + kk) : B;
@@ -115,8 +117,8 @@ template <class Cfg>
 __device__ __forceinline__ void gemm_load_part_hoisted(double* sdstA, double* sdstB, int64_t a_pass, int64_t b_pass,
                                                        const double* ap_kt, const double* bp_kt, int part) {
   constexpr int PARTS = Cfg::BK / 4;
-  constexpr int ACH = Cfg::BM / 2, AROWS = kThreads / ACH, APASS = Cfg::BK / AROWS;
-  constexpr int BCH = Cfg::BK / 2, BCOLS = kThreads / BCH, BPASS = Cfg::BN / BCOLS;
+  constexpr int ACH = Cfg::BM / 2, AROWS = Cfg::THREADS / ACH, APASS = Cfg::BK / AROWS;
+  constexpr int BCH = Cfg::BK / 2, BCOLS = Cfg::THREADS / BCH, BPASS = Cfg::BN / BCOLS;
 #pragma unroll
   for (int pp = 0; pp < APASS / PARTS; ++pp) {
     const int p = part * (APASS / PARTS) + pp;
@@ -189,7 +191,7 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
   // for each of its batches (the DMMA pipe idles during the epilogue).
   if (KT >= 2 && __isGlobal(d.Cin)) {
     constexpr int LPC = (Cfg::BM * 8 + 127) / 128;      // 128-byte lines per tile column
-    for (int x = tid; x < nrem * LPC; x += kThreads) {
+    for (int x = tid; x < nrem * LPC; x += Cfg::THREADS) {
       int col = x / LPC, seg = x - col * LPC;
       if (seg * 16 < mrem)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(d.Cin + (int64_t)col * d.ldcin + seg * 16));
@@ -202,7 +204,7 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
   if (next.valid && (next.lda != d.lda || next.ldb != d.ldb)) fn.kfull = 0;   // strides are shared below
   constexpr int ACH_ = Cfg::BM / 2, BCH_ = Cfg::BK / 2;
   const int64_t a_kt = (int64_t)Cfg::BK * d.lda;
-  const int64_t a_pass = (int64_t)(kThreads / ACH_) * d.lda, b_pass = (int64_t)(kThreads / BCH_) * d.ldb;
+  const int64_t a_pass = (int64_t)(Cfg::THREADS / ACH_) * d.lda, b_pass = (int64_t)(Cfg::THREADS / BCH_) * d.ldb;
   double* const sdA0 = smem + (tid / ACH_) * Cfg::LDA_S + 2 * (tid % ACH_);
   double* const sdB0 = smem + Cfg::A_STAGE + (tid / BCH_) * Cfg::LDB_S + 2 * (tid % BCH_);
 
