@@ -242,3 +242,22 @@ def test_bench_cli_csv(mla, capsys):  # reference test_bench.py: header, seed re
     assert bench_cli.main(["--gepp", "--n", "1024", "--sweep-b", "64:128:64"]) == 0
     out = capsys.readouterr().out.strip().splitlines()
     assert out[0] == "k,gflops" and len(out) == 3
+
+
+def test_distributed_driver_two_ranks_cuda_ops(mla):
+    """The multi-GPU driver end to end with its CUDA operator table and real broadcasts, 2 ranks sharing
+    the one GPU of this run (gloo rendezvous; no kernel waits on another rank's kernel).  The script
+    asserts pivot equality and the 1e-10 factor bound against the oracle on rank 0."""
+    import socket
+    import subprocess
+    import sys
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2", "--master-addr",
+                          "127.0.0.1", "--master-port", str(port), os.path.join(root, "tools", "dev_dist_check.py")],
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert out.stdout.count("pivots_equal=True") == 3
