@@ -56,7 +56,7 @@ def lib() -> ctypes.CDLL:
                                   ctypes.c_double, ctypes.c_double, _vp, _vp]
     L.mla_getrf_trace.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     L.mla_getrf_trace.restype = ctypes.c_int
-    L.mla_gemm_half_experiment.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp]
+    L.mla_gemm_half_experiment.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, ctypes.c_int, _vp]
     L.mla_gemm_half_experiment.restype = ctypes.c_int
     L.mla_getrf_debug.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64)]
     L.mla_getrf_debug.restype = ctypes.c_int

@@ -209,13 +209,54 @@ k_gemm_half(GemmProblem p, unsigned* ctrl) {
   }
 }
 
+// Same idea inside ONE 256-thread CTA: two independent 128-thread groups, each with its own ring and its
+// own named barrier, each pulling 128x64 half-tiles from the queue.
+__global__ void __launch_bounds__(kThreads, 1)
+k_gemm_dual(GemmProblem p, unsigned* ctrl) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_tile[2];
+  using Cfg = GemmHalfCfg;
+  const int g = grp_id<Cfg::THREADS>(), gtid = grp_tid<Cfg::THREADS>();
+  double* gsmem = smem + g * (Cfg::SMEM_BYTES / 8);
+  const int ntiles = gemm_num_tiles<Cfg>(p);
+  auto pop = [&]() {
+    if (gtid == 0) s_tile[g] = (int)atomicAdd(ctrl + CW_QUEUE_NEXT, 1u);
+    grp_sync<Cfg::THREADS>();
+    int t = s_tile[g];
+    grp_sync<Cfg::THREADS>();
+    return t;
+  };
+  int t = pop();
+  if (t >= ntiles) return;
+  TileDesc cur = gemm_tile_desc<Cfg>(p, t);
+  int base = 0;
+  tile_prologue<Cfg>(cur, base, gsmem);
+  while (true) {
+    int tn = pop();
+    TileDesc nxt{};
+    nxt.valid = false;
+    if (tn < ntiles && tile_kt<Cfg>(cur) >= Cfg::STAGES - 1) nxt = gemm_tile_desc<Cfg>(p, tn);
+    base = tile_run<Cfg>(cur, nxt, base, gsmem);
+    if (nxt.valid) { cur = nxt; continue; }
+    if (tn >= ntiles) break;
+    cur = gemm_tile_desc<Cfg>(p, tn);
+    base = 0;
+    tile_prologue<Cfg>(cur, base, gsmem);
+  }
+}
+
 extern "C" int mla_gemm_half_experiment(mla_handle h, double* C, int64_t m, int64_t n, int64_t ldc, const double* A,
-                                        int64_t lda, const double* B, int64_t ldb, int64_t k, void* stream) {
+                                        int64_t lda, const double* B, int64_t ldb, int64_t k, int mode, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   GemmProblem p{C, ldc, A, lda, B, ldb, (int)m, (int)n, (int)k, 1.0, -1.0};
   CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
-  CK(h, cudaFuncSetAttribute(k_gemm_half, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmHalfCfg::SMEM_BYTES));
-  k_gemm_half<<<2 * h->num_sms, 128, GemmHalfCfg::SMEM_BYTES, s>>>(p, h->ctrl);
+  if (mode == 0) {
+    CK(h, cudaFuncSetAttribute(k_gemm_half, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmHalfCfg::SMEM_BYTES));
+    k_gemm_half<<<2 * h->num_sms, 128, GemmHalfCfg::SMEM_BYTES, s>>>(p, h->ctrl);
+  } else {
+    CK(h, cudaFuncSetAttribute(k_gemm_dual, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * GemmHalfCfg::SMEM_BYTES));
+    k_gemm_dual<<<h->num_sms, kThreads, 2 * GemmHalfCfg::SMEM_BYTES, s>>>(p, h->ctrl);
+  }
   CK(h, cudaGetLastError());
   return MLA_OK;
 }

@@ -124,6 +124,21 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
+// ---- thread groups ---------------------------------------------------------------------------------
+// A routine templated on its thread count NT runs either on the whole CTA (NT == kThreads) or on one of
+// the CTA's independent groups of NT threads (group g = threadIdx.x / NT).  Groups synchronise on
+// their own named barrier (id 1 + g), never on barrier 0, so two groups of a CTA progress
+// independently -- one group's epilogue overlaps the other's DMMA stream.
+template <int NT>
+__device__ __forceinline__ int grp_tid() { return NT == kThreads ? (int)threadIdx.x : (int)(threadIdx.x % NT); }
+template <int NT>
+__device__ __forceinline__ int grp_id() { return NT == kThreads ? 0 : (int)(threadIdx.x / NT); }
+template <int NT>
+__device__ __forceinline__ void grp_sync() {
+  if (NT == kThreads) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / NT)), "n"(NT) : "memory");
+}
+
 __device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
 __device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
 

@@ -54,7 +54,7 @@ __device__ __forceinline__ void gemm_load_stage(double* smem, int slot, const do
   double* sA = smem + slot * Cfg::STAGE;
   double* sB = sA + Cfg::A_STAGE;
   const int k0 = kt * Cfg::BK;
-  const int tid = threadIdx.x;
+  const int tid = grp_tid<Cfg::THREADS>();
   if (AL16) {
     constexpr int ACH = Cfg::BM / 2;
     for (int c = tid; c < Cfg::BK * ACH; c += Cfg::THREADS) {
@@ -103,7 +103,7 @@ template <class Cfg, class Desc>
 __device__ __forceinline__ FastSrc<Cfg> make_fast_src(const Desc& d) {
   FastSrc<Cfg> f;
   constexpr int ACH = Cfg::BM / 2, BCH = Cfg::BK / 2;
-  const int tid = threadIdx.x;
+  const int tid = grp_tid<Cfg::THREADS>();
   const bool fast = Cfg::FAST_OK && d.valid && ((((uintptr_t)d.A | (uintptr_t)d.B) & 15) == 0) &&
                     ((d.lda & 1) == 0) && ((d.ldb & 1) == 0) && d.mrem >= Cfg::BM && d.nrem >= Cfg::BN;
   f.kfull = fast ? d.K / Cfg::BK : 0;
@@ -163,7 +163,7 @@ __device__ __forceinline__ void tile_issue(const TileDesc& d, int kt, int slot, 
 // Prime the ring for tile d: positions 0..STAGES-2 of its k-stream go to slots base.. .
 template <class Cfg>
 __device__ __forceinline__ void tile_prologue(const TileDesc& d, int base, double* smem) {
-  __syncthreads();  // previous user of the ring is done
+  grp_sync<Cfg::THREADS>();  // previous user of the ring is done
 #pragma unroll
   for (int s = 0; s < Cfg::STAGES - 1; ++s) tile_issue<Cfg>(d, s, (base + s) % Cfg::STAGES, smem);
 }
@@ -175,7 +175,7 @@ __device__ __forceinline__ void tile_prologue(const TileDesc& d, int base, doubl
 template <class Cfg>
 __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, double* smem) {
   constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES, NI = Cfg::NI, NJ = Cfg::NJ;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = grp_tid<Cfg::THREADS>(), lane = tid & 31, warp = tid >> 5;
   const int wi = warp % Cfg::WI, wj = warp / Cfg::WI;
   const int g = lane >> 2, q = lane & 3;
   const int mrem = imin(d.mrem, Cfg::BM), nrem = imin(d.nrem, Cfg::BN);
@@ -210,7 +210,7 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
 
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
-    __syncthreads();
+    grp_sync<Cfg::THREADS>();
     const int pos = kt + STAGES - 1;
     const int lslot = (base + pos) % STAGES;
     const bool cur_tile = pos < KT;
