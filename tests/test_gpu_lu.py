@@ -261,3 +261,49 @@ def test_distributed_driver_two_ranks_cuda_ops(mla):
                          capture_output=True, text=True, timeout=600, cwd=root)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert out.stdout.count("pivots_equal=True") == 3
+
+
+def test_random_small_shapes_property(mla):
+    """Property sweep in the spirit of the reference's hypothesis tests (test_lu.py:247-256,
+    test_kernels.py:366-401): random small m >= n, block widths and variants; pivots identical to the
+    oracle, factors within the parity bound, backward error bounded."""
+    rng = np.random.default_rng(2024)
+    for trial in range(60):
+        n = int(rng.integers(1, 41))
+        m = n + int(rng.integers(0, 25))
+        b_i = int(rng.integers(1, 9))
+        b_o = b_i * int(rng.integers(1, 5))
+        variant = VARIANTS[int(rng.integers(0, len(VARIANTS)))]
+        a = np.asfortranarray(rng.standard_normal((m, n)))
+        if trial % 7 == 0 and n > 2:
+            a[:, int(rng.integers(0, n))] = 0.0          # a structurally singular column now and then
+        if trial % 5 == 0 and n > 3:
+            a[int(rng.integers(0, m)), :] *= 1e6          # badly scaled row
+        run_and_check(mla, a, b_o, b_i, variant, t_pf=int(rng.integers(1, 40)),
+                      what=f"trial {trial}: {m}x{n} b={b_o}/{b_i} {variant}")
+
+
+def test_operator_property_sweep(mla):
+    """Random laswp round trips / involutions and trsm-multiply-back on odd shapes and views."""
+    rng = np.random.default_rng(7)
+    for trial in range(25):
+        rows, cols = int(rng.integers(1, 300)), int(rng.integers(1, 70))
+        npiv = int(rng.integers(1, rows + 1))
+        parent = mla.alloc_matrix(rows + 5, cols + 3)
+        a = np.asfortranarray(rng.standard_normal((rows, cols)))
+        view = parent[2:2 + rows, 1:1 + cols]
+        view.copy_(mla.from_numpy(a))
+        ipiv = np.array([rng.integers(t, rows) for t in range(npiv)], dtype=np.int64)
+        mla.laswp(view, ipiv)
+        ref = a.copy(order="F")
+        oracle.laswp(ref, ipiv)
+        assert np.array_equal(mla.to_numpy(parent)[2:2 + rows, 1:1 + cols], ref)
+        mla.laswp(view, ipiv, reverse=True)
+        assert np.array_equal(mla.to_numpy(parent)[2:2 + rows, 1:1 + cols], a)
+        w, c = int(rng.integers(1, 150)), int(rng.integers(1, 200))
+        low = np.asfortranarray(rng.uniform(-1, 1, (w, w)))
+        x = np.asfortranarray(rng.standard_normal((w, c)))
+        dx = mla.from_numpy(x)
+        mla.trsm_llu(mla.from_numpy(low), dx)
+        back = (np.tril(low, -1) + np.eye(w)) @ mla.to_numpy(dx)
+        assert np.abs(back - x).max() <= 64 * w * EPS * max(1.0, np.abs(mla.to_numpy(dx)).max())
