@@ -316,6 +316,8 @@ __device__ void gemm_tile(const double* __restrict__ A, int64_t lda, const doubl
   tile_run<Cfg>(d, none, 0, smem);
 }
 
+constexpr int kRowBlockTiles = 64;   // row tiles per L2 row block of the tile order
+
 // A whole C := alpha*C + beta*A@B problem as a list of BM x BN tiles, column-strip major
 // (consecutive tile ids walk down the rows of one BN-wide column strip, so the k x BN strip of B
 // and the strip's prepare step are shared by neighbours in the queue).
@@ -334,8 +336,17 @@ __device__ __forceinline__ int gemm_num_tiles(const GemmProblem& p) {
 
 template <class Cfg>
 __device__ __forceinline__ TileDesc gemm_tile_desc(const GemmProblem& p, int t) {
+  // Row-block-major order: the row tiles are cut into blocks of kRowBlockTiles; inside a block the
+  // tiles go strip by strip.  The A rows of one block (kRowBlockTiles x BM x k doubles, 16 MiB at
+  // k = 256) then stay in L2 while every column strip passes over them, instead of the whole m x k
+  // operand being re-read from HBM for every strip.
   const int tm_count = (p.m + Cfg::BM - 1) / Cfg::BM;
-  const int tm = t % tm_count, tn = t / tm_count;
+  const int tn_count = (p.n + Cfg::BN - 1) / Cfg::BN;
+  const int per_block = kRowBlockTiles * tn_count;
+  const int rb = t / per_block;
+  const int rows_here = imin(kRowBlockTiles, tm_count - rb * kRowBlockTiles);
+  const int r = t - rb * per_block;
+  const int tn = r / rows_here, tm = rb * kRowBlockTiles + (r - tn * rows_here);
   const int i0 = tm * Cfg::BM, j0 = tn * Cfg::BN;
   double* c = p.C + (int64_t)j0 * p.ldc + i0;
   return TileDesc{p.A + i0, p.lda, p.B + (int64_t)j0 * p.ldb, p.ldb, c, p.ldc, c, p.ldc,

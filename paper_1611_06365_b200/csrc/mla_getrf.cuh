@@ -81,7 +81,8 @@ struct IterShape {
   int nps, tmc;                      // panel strips, row tiles
   int pq_prep, pq_total;
   int rcols, nrs, rq_prep, rq_gemm, nleft, rq_total;
-  int la_strips, gs;                 // PREP lookahead (strips) and RQ group size
+  int la_strips, gs;                 // PREP lookahead (strips) and RQ group size of the first row block
+  int rb0;                           // row tiles of the first row block (<= kRowBlockTiles)
 };
 
 __device__ __forceinline__ IterShape iter_shape(const LuState* st, int m, int n, int grid) {
@@ -107,11 +108,14 @@ __device__ __forceinline__ IterShape iter_shape(const LuState* st, int m, int n,
   // strip s]; then the LEFT strips that did not fit a group.  PREP and LEFT are HBM-bound row
   // interchanges (+ a small trsm): spread between the tensor-bound GEMM tiles they overlap with them
   // instead of saturating the memory system all at once at the start of the iteration.
+  // Row-block-major tile order (see gemm_tile_desc): the first block of kRowBlockTiles row tiles
+  // carries the PREP/LEFT items of the groups; the later blocks are pure GEMM groups.
   s.rq_prep = 0;
-  s.gs = s.tmc + 2;
+  s.rb0 = imin(kRowBlockTiles, s.tmc);
+  s.gs = s.rb0 + 2;
   s.rq_gemm = s.nrs * s.tmc;
   s.nleft = (s.q0 + LEFT_CW - 1) / LEFT_CW;
-  s.rq_total = s.nrs * s.gs + imax(0, s.nleft - s.nrs);
+  s.rq_total = s.nrs * (s.tmc + 2) + imax(0, s.nleft - s.nrs);
   return s;
 }
 
@@ -205,8 +209,8 @@ __device__ __forceinline__ QItem decode_item(const IterShape& s, int which, int 
     else { int g = t - s.pq_prep; q.kind = 3; q.strip = g / s.tmc; q.tm = g - q.strip * s.tmc; }
     return q;
   }
-  const int ngrp = s.nrs * s.gs;
-  if (t < ngrp) {
+  const int ngrp0 = s.nrs * s.gs;          // first row block: [PREP][LEFT][rb0 tiles] per strip
+  if (t < ngrp0) {
     const int grp = t / s.gs, slot = t - grp * s.gs;
     if (slot == 0) {
       int ps = grp + s.la_strips;
@@ -216,8 +220,21 @@ __device__ __forceinline__ QItem decode_item(const IterShape& s, int which, int 
     } else { q.kind = 3; q.strip = grp; q.tm = slot - 2; }
     return q;
   }
+  int r = t - ngrp0;
+  const int later = s.nrs * (s.tmc - s.rb0);   // GEMM tiles of the later row blocks
+  if (r < later) {
+    const int per_block = s.nrs * kRowBlockTiles;
+    const int rb = r / per_block;              // 0 = second row block
+    const int row0 = s.rb0 + rb * kRowBlockTiles;
+    const int rows_here = imin(kRowBlockTiles, s.tmc - row0);
+    r -= rb * per_block;
+    q.kind = 3;
+    q.strip = r / rows_here;
+    q.tm = row0 + (r - q.strip * rows_here);
+    return q;
+  }
   q.kind = 4;
-  q.strip = s.nrs + (t - ngrp);
+  q.strip = s.nrs + (r - later);
   return q;
 }
 
