@@ -29,6 +29,12 @@ sys.path.insert(0, ROOT)
 
 from paper_1611_06365_b200.workloads import CONFIGS, flops_lu, make_matrix  # noqa: E402
 
+# DRAM bytes of ONE k_getrf launch on the default workload (n=32768, b=256/32, lu_et), from
+# `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` (profiles/r01_getrf_n32768_traffic.csv):
+# 577.2 GB read + 423.0 GB written; the algorithmic minimum (the trailing matrix read and written once
+# per iteration) is 2 * 8 * n^3 / (3 b) = 733 GB.
+DEFAULT_WORKLOAD_DRAM_BYTES = 577163462144 + 423019379968
+
 FP64_TENSOR_PEAK_TFLOPS = 37.0   # measured on this pool's B200: tools/fp64_peak.cu (DMMA.8x8x4
                                  # issue-bound, 3 s sustained) -> profiles/r01_fp64_peak.log.
                                  # MEASURED_PEAKS.json has no FP64 entry.
@@ -375,7 +381,9 @@ def run_ours(args):
                    "et_events": res.et_events, "ws_joins": res.ws_joins, "panels": len(res.widths),
                    "gen_seconds": round(gen_s, 1)},
         "roofline": {"bound": "tensor", "achieved": round(val / 1e3, 3), "peak": FP64_TENSOR_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": round(val / 1e3 / FP64_TENSOR_PEAK_TFLOPS, 4), "traffic": None,
+                     "unit": "TFLOP/s", "frac": round(val / 1e3 / FP64_TENSOR_PEAK_TFLOPS, 4),
+                     "traffic": DEFAULT_WORKLOAD_DRAM_BYTES if (name == "config4" and n == 32768 and b_o == 256
+                                                                and args.variant == "lu_et") else None,
                      "kernel": "k_getrf (persistent; algorithmic flops 2n^3/3 per launch)",
                      "peak_source": "measured: DMMA.8x8x4 issue-bound rate, tools/fp64_peak.cu, "
                                     "profiles/r01_fp64_peak.log (MEASURED_PEAKS.json has no FP64 entry)"},
