@@ -122,6 +122,14 @@ int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_
                       int32_t* ipiv_host, int b_outer, int b_inner, int variant, int sm_pf,
                       int q_chunks, mla_lu_info* info_host);
 
+/* One update step of the multi-GPU driver as a single persistent launch: apply the broadcast panel P
+ * (rows x w: unit-lower L11 on top of L21, leading dimension ldp) with its w panel-local pivots to the
+ * column block T (rows x cols view starting at the panel's first row):
+ *   T := interchanges(T);  T[0:w] := trilu(L11)^-1 T[0:w];  T[w:] -= L21 * T[0:w]
+ * (laswp -> trsm_llu -> gemm_malleable of lu.py:251-253, 280-281, 289, 306-308).  Asynchronous. */
+int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
+                    int64_t cols, int64_t ldt, const int32_t* ipiv, void* stream);
+
 /* fill_random(a, seed) -- matrix.py:44-63: SplitMix64 stream, bit-identical to the reference;
  * value = scale*u + shift with u in (0,1) (scale=1, shift=0 reproduces fill_random; 2,-1 gives the
  * uniform[-1,1] configs).  col0/total_rows select a column block of a larger matrix (multi-GPU).

@@ -47,6 +47,7 @@ struct mla_handle_s {
   int32_t* ipiv_dev;
   size_t ipiv_dev_n;
   double* resid_dev;
+  unsigned apply_tag;    // per-call tag of the strip flags used by mla_apply_panel (never reused)
 };
 
 #define CK(h, call)                                   \
@@ -87,6 +88,7 @@ extern "C" int mla_create(int device, mla_handle* out) {
   cudaMemset(h->plan, 0, sizeof(PivPlan));
   cudaMemset(h->panel_ws, 0, sizeof(PanelWs));
   cudaMemset(h->lu_state, 0, sizeof(LuState));
+  h->apply_tag = 0x40000000u;   // far above any iteration number the persistent kernel tags flags with
   *out = h;
   return MLA_OK;
 }
@@ -528,6 +530,96 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
   rc = check_abort(h, s);
   if (info_host) *info_host = *h->info_host;
   return rc;
+}
+
+// ---- apply one factored panel to a block of columns (multi-GPU update step) ------------------------
+// The per-iteration update of the 1-D block-cyclic driver (distributed.py) as ONE persistent launch:
+//   T (rows x cols, the owned columns right of the panel, view starting at the panel's first row)
+//   P (rows x w, the broadcast panel: unit-lower L11 on top of L21), ipiv (w panel-local pivots)
+//   T := interchanges(T);  T[0:w] := trilu(L11)^-1 T[0:w];  T[w:] -= L21 @ T[0:w]
+// i.e. laswp -> trsm_llu -> gemm_malleable of lu.py:251-253, 280-281 / 289, 306-308, with the same
+// work-queue structure as the single-GPU kernel: PREP strips first, GEMM tiles (row-block-major,
+// chained) wait on their strip's release/acquire flag.  The plan comes from k_laswp_plan.
+struct ApplyArgs {
+  const double* P; int64_t ldp; int rows, w;
+  double* T; int64_t ldt; int cols;
+  PivPlan* plan; unsigned* ctrl; unsigned* flags; unsigned tag;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  const int nstrips = (a.cols + TRSM_CW - 1) / TRSM_CW;
+  const int rows_below = a.rows - a.w;
+  const int tmc = (rows_below + GemmUpdateCfg::BM - 1) / GemmUpdateCfg::BM;
+  const int total = nstrips + nstrips * tmc;
+  unsigned* next = a.ctrl + CW_QUEUE_NEXT;
+  auto decode = [&](int t, int& strip, int& tm) {   // GEMM items, row-block-major (see gemm_tile_desc)
+    const int g = t - nstrips;
+    const int per_block = kRowBlockTiles * nstrips;
+    const int rb = g / per_block;
+    const int rows_here = imin(kRowBlockTiles, tmc - rb * kRowBlockTiles);
+    const int r = g - rb * per_block;
+    strip = r / rows_here;
+    tm = rb * kRowBlockTiles + (r - strip * rows_here);
+  };
+  auto desc = [&](int strip, int tm) {
+    const int c0 = strip * TRSM_CW, i0 = a.w + tm * GemmUpdateCfg::BM;
+    double* c = a.T + (int64_t)c0 * a.ldt + i0;
+    return TileDesc{a.P + i0, a.ldp, a.T + (int64_t)c0 * a.ldt, a.ldt, c, a.ldt, c, a.ldt,
+                    a.w, a.rows - i0, imin(TRSM_CW, a.cols - c0), 1.0, -1.0, true};
+  };
+  int base = 0, ready_strip = -1;
+  bool primed = false;
+  int t = pop_item(next);
+  while (t < total) {
+    if (t < nstrips) {
+      const int c0 = t * TRSM_CW, cw = imin(TRSM_CW, a.cols - c0);
+      laswp_apply_cols(a.T + (int64_t)c0 * a.ldt, a.ldt, cw, a.plan->ref(), smem, kLaswpBufDoubles);
+      trsm_strip(a.P, a.w, a.ldp, a.T + (int64_t)c0 * a.ldt, cw, a.ldt, smem);
+      __syncthreads();
+      if (threadIdx.x == 0) { __threadfence(); st_release(&a.flags[t], a.tag); }
+      primed = false;
+      t = pop_item(next);
+      continue;
+    }
+    int strip, tm;
+    decode(t, strip, tm);
+    TileDesc cur = desc(strip, tm);
+    if (!primed) {
+      if (strip != ready_strip && !wait_flag_eq(&a.flags[strip], a.tag, a.ctrl + CW_ABORT)) return;
+      ready_strip = strip;
+      base = 0;
+      tile_prologue<GemmUpdateCfg>(cur, base, smem);
+    }
+    const int tn = pop_item(next);
+    TileDesc nxt{};
+    nxt.valid = false;
+    if (tn < total && tn >= nstrips && tile_kt<GemmUpdateCfg>(cur) >= GemmUpdateCfg::STAGES - 1) {
+      int s2, m2;
+      decode(tn, s2, m2);
+      if (s2 == ready_strip || flag_ready(&a.flags[s2], a.tag)) { ready_strip = s2; nxt = desc(s2, m2); }
+    }
+    base = tile_run<GemmUpdateCfg>(cur, nxt, base, smem);
+    primed = nxt.valid;
+    t = tn;
+  }
+}
+
+extern "C" int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
+                               int64_t cols, int64_t ldt, const int32_t* ipiv, void* stream) {
+  if (!h || rows < w || w < 0 || cols < 0 || (rows > 0 && (ldp < rows || ldt < rows))) return MLA_E_INVALID;
+  if (w > kMaxPiv || cols > (int64_t)kMaxStrips * TRSM_CW) return MLA_E_INVALID;
+  if (w == 0 || cols == 0) return MLA_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_laswp_plan<<<1, 32, 0, s>>>(ipiv, (int)w, rows, 0, h->plan, h->ctrl);
+  CK(h, cudaGetLastError());
+  CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
+  CK(h, cudaFuncSetAttribute(k_apply_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
+  ApplyArgs a{P, ldp, (int)rows, (int)w, T, ldt, (int)cols, h->plan, h->ctrl, h->lu_state->rprep_done, ++h->apply_tag};
+  void* args[] = {&a};
+  int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
+  CK(h, cudaLaunchCooperativeKernel((void*)k_apply_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
+  return MLA_OK;
 }
 
 // ---- fill_random -----------------------------------------------------------------------------------

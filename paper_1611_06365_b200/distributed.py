@@ -98,6 +98,10 @@ class CudaOps:
         self._m.fill_random(a, seed, scale, shift, row_scale=row_scale, col0=col0, total_rows=total_rows,
                             pool=self.pool)
 
+    def apply_panel(self, panel, w, target, piv):
+        """laswp + trsm + gemm of one update step as ONE persistent launch (no host sync)."""
+        self._k.apply_panel(panel, w, target, piv, pool=self.pool)
+
 
 class DistLU:
     """One rank's share of a block-cyclic LU.  `group` = process group (default WORLD)."""
@@ -197,6 +201,10 @@ class DistLU:
             return
         j0, w = k * self.b, self.map.width(k)
         tgt = self.a[j0:, col_lo:col_hi]
+        if hasattr(self.ops, "apply_panel"):
+            self.ops.apply_panel(panel, w, tgt, piv)
+            self.launches_per_factor += 2
+            return
         self.ops.laswp(tgt, piv)
         self.ops.trsm(panel[:w, :w], tgt[:w, :])
         if self.n - j0 - w > 0:

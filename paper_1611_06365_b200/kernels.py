@@ -88,3 +88,19 @@ def laswp(a: torch.Tensor, piv, team=None, reverse: bool = False, pool=None, che
     fn = _capi.lib().mla_laswp if check else _capi.lib().mla_laswp_async   # async: no host sync
     _capi.check(fn(pool.handle, a.data_ptr(), rows, cols, ld, ip.data_ptr(), npiv,
                    int(bool(reverse)), _stream(a)), pool.handle, "laswp")
+
+
+def apply_panel(panel: torch.Tensor, w: int, target: torch.Tensor, piv, pool=None) -> None:
+    """One update step of the block-cyclic driver as a single persistent launch: interchanges, trsm with
+    the panel's unit-lower top block and the rank-w update of `target` (rows x cols, same first row as
+    the panel) -- laswp + trsm_llu + gemm_malleable of the reference's lu.py:251-253, 280-281 fused."""
+    rows, pw, ldp = check_colmajor(panel, "panel")
+    trows, cols, ldt = check_colmajor(target, "target")
+    if trows != rows or w > pw or w > rows:
+        raise ValueError("apply_panel: panel/target shapes disagree")
+    ip = _device_pivots(piv, target.device)
+    if int(ip.shape[0]) < w:
+        raise ValueError("apply_panel: need w pivots")
+    pool = pool or default_pool(target.device.index)
+    _capi.check(_capi.lib().mla_apply_panel(pool.handle, panel.data_ptr(), rows, w, ldp, target.data_ptr(), cols,
+                                            ldt, ip.data_ptr(), _stream(target)), pool.handle, "apply_panel")
