@@ -5,13 +5,19 @@
 //                       (panel_ll, collective over the team),
 //   CTAs [sm_pf, G)   = team RU: pull work items of the trailing update from atomic queues.
 //
-// Per outer iteration the work is cut into items, executed from two queues in this order:
-//   PQ (next panel's columns [q1, q1+w)):  PREP strips (row interchanges of the previous panel +
-//        trsm with A11, lu.py:251-253,280), then GEMM tiles of A22p (lu.py:281);
-//   RQ (remainder [q1+w, n) and the left part): PREP strips (lu.py:251-253,289), GEMM tiles of A22r
-//        (lu.py:306-308), LEFT strips (row interchanges of the L part, lu.py:252).
+// Per outer iteration the work is cut into items (PREP of a 128-column strip = row interchanges of
+// the previous panel + trsm with A11, lu.py:251-253,280,289; GEMM = one 128x128 tile of A22 -= A21@A12,
+// lu.py:281,306-308; LEFT = interchanges of 256 columns of the L part, lu.py:252) in two atomic queues:
+//   PQ: [PREP of the next panel's strips][PREP of the first ~G remainder strips -- fillers that keep
+//        every CTA busy while the panel PREP runs][GEMM tiles of the next panel's columns];
+//   RQ: first row block (64 row tiles): per remainder strip s a group [PREP of strip s+lookahead]
+//        [LEFT strip s][the strip's GEMM tiles of that row block]; then the later row blocks as pure
+//        GEMM groups (row-block-major order keeps a block's A21 rows in L2 across all strips); then
+//        leftover LEFT strips.  The HBM-bound interchanges thus run between tensor-bound tiles.
 // Every CTA first helps to drain PQ (it is the critical path to the next panel); PF CTAs then wait
-// for PQ to complete and run the panel while RU CTAs drain RQ.
+// for PQ to complete and run the panel while RU CTAs drain RQ.  Pops run one item ahead (two on long
+// queues, with an atomic whose round trip overlaps the running tile) so that consecutive GEMM tiles
+// chain through the tile engine; completion is counted once per CTA.
 //
 //   WS  (lu_mb / lu_et, pool.py:377-414): a PF CTA that returns from the panel -- i.e. after the
 //        panel team's final barrier, so the donor team has fully quiesced -- simply starts pulling

@@ -2,7 +2,9 @@
 // CTAs (reference lu.py:140-180 lu_blk_ll + lu.py:44-72 _unb_pivoted).
 //
 // Per inner block [j, j+wb) of the m x w panel (wb = b_inner):
-//   1. U block:  P[0:j, j:j+wb] = trilu(P[0:j,0:j])^-1 P[0:j, j:j+wb]        (trsm_strip, rank 0)
+//   1. U block:  P[0:j, j:j+wb] = trilu(P[0:j,0:j])^-1 P[0:j, j:j+wb]  (lu.py:166) -- in the reference's
+//      left-looking order this is a trsm per block (stand-alone lu_blk_ll: columns dealt to the first
+//      CTAs); inside the persistent kernel (eager_u) it is already there, see 4b.
 //   2. rows [j, m) are dealt to the team in contiguous slabs (one per CTA, like the reference's
 //      _share, kernels.py:28-32); each CTA updates its slab with one DMMA gemm
 //         S = P[slab, j:j+wb] - P[slab, 0:j] @ U                               (lu.py:167-168)
@@ -10,13 +12,17 @@
 //   3. wb pivot steps on the slab (lu.py:48-71).  Each step costs ONE team-wide exchange through
 //      global memory: every CTA publishes its local arg-max candidate (value, row -- lowest row
 //      wins ties, lu.py:53 -- and that row's wb values), the CTA owning the diagonal row publishes
-//      that row; after an acquire-poll of all slots every CTA knows the pivot row p, swaps its side
-//      of (j+c <-> p), divides by the pivot (division, lu.py:65-67) and applies the rank-1 update
+//      that row (16-byte self-validating words, no fences); after polling all slots every CTA knows
+//      the pivot row p, swaps its side of (j+c <-> p), forms the multipliers (lu.py:65-67) and applies
+//      the rank-1 update
 //      while already searching the next column's maximum.  An exactly-zero column records piv = j+c,
 //      raises the singular flag and is skipped (lu.py:56-59).
 //   4. the block's wb interchanges are applied to the other panel columns as one parallel
 //      permutation plan (equivalent data movement to lu.py:165,173-174,178; applying them eagerly
 //      to the right-hand columns as well means an ET cut needs no extra pass).
+//   4b. eager_u (Crout order): the rows of U this block determines are computed for ALL later panel
+//      columns (one DMMA row-block step per 32 rows), which removes the per-block trsm chain and lets
+//      an ET cut hand over leftover columns that already hold their A12 rows.
 //   5. ET poll: once per completed block while columns remain (lu.py:177).
 //
 // Row indices / pivots are panel-local (lu.py:175).
