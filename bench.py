@@ -29,11 +29,12 @@ sys.path.insert(0, ROOT)
 
 from paper_1611_06365_b200.workloads import CONFIGS, flops_lu, make_matrix  # noqa: E402
 
-# DRAM bytes of ONE k_getrf launch on the default workload (n=32768, b=256/32, lu_et), from
+# DRAM bytes of ONE k_getrf launch on the default workload (n=32768, b=512/64, lu_et, sm_pf 32), from
 # `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` (profiles/r01_getrf_n32768_traffic.csv):
-# 577.2 GB read + 423.0 GB written; the algorithmic minimum (the trailing matrix read and written once
-# per iteration) is 2 * 8 * n^3 / (3 b) = 733 GB.
-DEFAULT_WORKLOAD_DRAM_BYTES = 577163462144 + 423019379968
+# 480.6 GB read + 237.3 GB written; the algorithmic minimum (the trailing matrix read and written once
+# per iteration) is 2 * 8 * n^3 / (3 b) = 367 GB at b = 512 (ET cuts make the effective b smaller).
+# At b=256/32 the same measurement gave 577.2 + 423.0 GB against a minimum of 733 GB.
+DEFAULT_WORKLOAD_DRAM_BYTES = 480622493952 + 237251566592
 
 FP64_TENSOR_PEAK_TFLOPS = 37.0   # measured on this pool's B200: tools/fp64_peak.cu (DMMA.8x8x4
                                  # issue-bound, 3 s sustained) -> profiles/r01_fp64_peak.log.
@@ -152,8 +153,15 @@ def pick(args, world):
     name = args.config or ("config4" if world == 1 else "config5")
     cfg = CONFIGS[name]
     n = args.n or cfg.n
-    b_o = args.b_outer or cfg.b_outer
-    b_i = args.b_inner or (cfg.b_inner if args.b_outer is None else max(1, b_o // 8))
+    default_b = cfg.b_outer
+    if name == "config4" and args.b_outer is None:
+        # config 4 is a block-size sweep b in {128, 256, 512, 768} with inner block b/8; the headline
+        # line uses the best point of the sweep on B200 (profiles/r01_bench_config4_bsweep.json)
+        default_b = 512
+        if args.sm_pf is None:
+            args.sm_pf = 32
+    b_o = args.b_outer or default_b
+    b_i = args.b_inner or (cfg.b_inner if b_o == cfg.b_outer else max(1, b_o // 8))
     return name, cfg, n, b_o, b_i
 
 
@@ -382,7 +390,7 @@ def run_ours(args):
                    "gen_seconds": round(gen_s, 1)},
         "roofline": {"bound": "tensor", "achieved": round(val / 1e3, 3), "peak": FP64_TENSOR_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": round(val / 1e3 / FP64_TENSOR_PEAK_TFLOPS, 4),
-                     "traffic": DEFAULT_WORKLOAD_DRAM_BYTES if (name == "config4" and n == 32768 and b_o == 256
+                     "traffic": DEFAULT_WORKLOAD_DRAM_BYTES if (name == "config4" and n == 32768 and b_o == 512
                                                                 and args.variant == "lu_et") else None,
                      "kernel": "k_getrf (persistent; algorithmic flops 2n^3/3 per launch)",
                      "peak_source": "measured: DMMA.8x8x4 issue-bound rate, tools/fp64_peak.cu, "
