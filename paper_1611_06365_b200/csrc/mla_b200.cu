@@ -175,6 +175,7 @@ k_gemm(GemmProblem p, unsigned* ctrl, const unsigned* join_flag, int donors) {
     if (!nxt.valid) break;
     cur = nxt;
   }
+  bulk_wait_all();   // this CTA's reductions into C are performed before the kernel retires
 }
 
 // EXPERIMENT (tools/dev_gemm_half.py): the same tile engine as 128-thread CTAs on 128x64 tiles, two CTAs
@@ -209,6 +210,7 @@ k_gemm_half(GemmProblem p, unsigned* ctrl) {
     base = 0;
     tile_prologue<Cfg>(cur, base, smem);
   }
+  bulk_wait_all();
 }
 
 // Same idea inside ONE 256-thread CTA: two independent 128-thread groups, each with its own ring and its
@@ -245,6 +247,7 @@ k_gemm_dual(GemmProblem p, unsigned* ctrl) {
     base = 0;
     tile_prologue<Cfg>(cur, base, gsmem);
   }
+  bulk_wait_all();
 }
 
 extern "C" int mla_gemm_half_experiment(mla_handle h, double* C, int64_t m, int64_t n, int64_t ldc, const double* A,
@@ -603,6 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
     primed = nxt.valid;
     t = tn;
   }
+  bulk_wait_all();
 }
 
 extern "C" int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,

@@ -131,6 +131,20 @@ __device__ __forceinline__ void gemm_load_part_hoisted(double* sdstA, double* sd
   }
 }
 
+// ---- bulk asynchronous reduction (TMA engine): global[dst] += shared[src] in L2 ----------------------
+// Used by the LU update's epilogue: C -= A@B becomes "stage -acc in shared memory, let the TMA engine
+// add it into C", so the SM neither reads C nor waits for it and moves straight on to the next tile.
+__device__ __forceinline__ void bulk_red_add_f64(double* gdst, const double* ssrc, unsigned bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;"
+               ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// all bulk reductions issued by this thread have been performed (their results are in L2 / global)
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+constexpr int RED_LDS = 136;   // doubles per staged column (1088 B: conflict-free STS.128, 16-B aligned)
+
 // Description of one C tile for the pipelined tile engine.
 struct TileDesc {
   const double* A; int64_t lda;       // mrem x K
@@ -198,6 +212,10 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
     }
   }
 
+  // the previous tile's epilogue may still be reading its staged accumulators out of the ring slot this
+  // tile's first load will overwrite
+  if constexpr (Cfg::FAST_OK) bulk_wait_read0();
+
   // fast-path constants of this tile and of the prefetched successor, hoisted out of the k loop
   const FastSrc<Cfg> fd = make_fast_src<Cfg>(d);
   FastSrc<Cfg> fn = make_fast_src<Cfg>(next);
@@ -253,7 +271,42 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
   const int64_t ldcin = d.ldcin, ldcout = d.ldcout;
   const bool vec = ((((uintptr_t)Cin | (uintptr_t)Cout) & 15) == 0) && ((ldcin & 1) == 0) && ((ldcout & 1) == 0);
   const bool full = vec && mrem == Cfg::BM && nrem == Cfg::BN;
-  if (full) {
+  bool red_done = false;
+  if constexpr (Cfg::FAST_OK && Cfg::BM == 128 && Cfg::BN == 128 && Cfg::WJ == 4) {
+    if (full && alpha == 1.0 && beta == -1.0 && Cin == Cout && KT > 0 && __isGlobal(Cout)) {
+      // C -= acc through the TMA engine: -acc is staged, half a tile (64 columns) at a time, in the ring
+      // slot this tile consumed last, and added into C by one 1-KiB bulk reduction per column.
+      double* stg = smem + ((base + KT - 1) % STAGES) * Cfg::STAGE;
+      static_assert(64 * RED_LDS <= Cfg::STAGE, "staging fits one ring slot");
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        if ((wj >> 1) == half) {
+#pragma unroll
+          for (int a = 0; a < NJ; ++a) {
+            double* sp = stg + ((wj & 1) * Cfg::WTJ + a * 8 + g) * RED_LDS + wi * Cfg::WTI + 2 * q;
+#pragma unroll
+            for (int b = 0; b < NI; ++b)
+              *reinterpret_cast<double2*>(sp + b * 8) = make_double2(-acc[a][b][0], -acc[a][b][1]);
+          }
+        }
+        fence_proxy_async_smem();
+        grp_sync<Cfg::THREADS>();
+        if (tid < 64) {
+          bulk_red_add_f64(Cout + (int64_t)(half * 64 + tid) * ldcout, stg + tid * RED_LDS, Cfg::BM * 8);
+          bulk_commit();
+          if (half == 0) bulk_wait_read0();   // the second half reuses the staging area
+        }
+        if (half == 0) grp_sync<Cfg::THREADS>();
+      }
+      if (!next.valid) {            // somebody else will use this shared memory next
+        if (tid < 64) bulk_wait_read0();
+        grp_sync<Cfg::THREADS>();
+      }
+      red_done = true;
+    }
+  }
+  if (red_done) {
+  } else if (full) {
 #pragma unroll
     for (int a = 0; a < NJ; ++a) {
       int j = wj * Cfg::WTJ + a * 8 + g;

@@ -347,7 +347,9 @@ __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* 
   }
   // Completion is reported once per CTA, when it finds the queue empty: a per-item fence + atomic
   // would stall the tile pipeline for two L2 round trips per tile.  The CTA whose report completes
-  // the count announces RU done (lu.py:309-310).
+  // the count announces RU done (lu.py:309-310).  The tiles' bulk reductions into C must have been
+  // performed before the report.
+  bulk_wait_all();
   __syncthreads();
   if (threadIdx.x == 0 && executed > 0) {
     __threadfence();
