@@ -6,6 +6,8 @@ Names kept from the reference (pkg/src/mla/__init__.py:6-33): lu_la, lu_blk_ll, 
 trsm_llu, gemm_malleable, laswp, LuResult, PivotVector, Policy, BlockConfig (+ the matrix helpers).
 """
 from .config import VARIANTS, BlockConfig, CacheConfig, Policy
+from .costmodel import (cumulative_flop_share, flops_ll_partial, flops_panel_total, flops_rl_partial,
+                        iteration_flops, schedule_flops)
 from .kernels import gemm_malleable, laswp, trsm_llu
 from .lu import (CountingStop, LuResult, et_schedule_from, et_widths_from, lu_blk_ll, lu_blk_rl,
                  lu_la, lu_unb)
@@ -24,5 +26,6 @@ __all__ = [
     "et_schedule_from", "et_widths_from", "fill_random", "flops_lu", "frobenius_norm", "from_numpy",
     "gemm_malleable", "laswp", "leading_dimension", "lu_blk_ll", "lu_blk_rl", "lu_la", "lu_unb",
     "make_config_matrix", "make_matrix", "partition_2x2", "residual_lu", "residual_packed",
-    "signal_complete", "split_lu", "swap_rows", "to_numpy", "trsm_llu",
+    "cumulative_flop_share", "flops_ll_partial", "flops_panel_total", "flops_rl_partial",
+    "iteration_flops", "schedule_flops", "signal_complete", "split_lu", "swap_rows", "to_numpy", "trsm_llu",
 ]
