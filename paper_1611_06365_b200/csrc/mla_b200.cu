@@ -76,7 +76,7 @@ extern "C" int mla_create(int device, mla_handle* out) {
   if (cudaMalloc(&h->ctrl, CW_COUNT * sizeof(unsigned)) != cudaSuccess) { delete h; return MLA_E_CUDA; }
   if (cudaMallocHost(&h->ctrl_host, CW_COUNT * sizeof(unsigned)) != cudaSuccess) { cudaFree(h->ctrl); delete h; return MLA_E_CUDA; }
   cudaMemset(h->ctrl, 0, CW_COUNT * sizeof(unsigned));
-  bool ok = cudaMalloc(&h->plan, sizeof(PivPlan)) == cudaSuccess &&
+  bool ok = cudaMalloc(&h->plan, 2 * sizeof(PivPlan)) == cudaSuccess &&
             cudaMalloc(&h->panel_ws, sizeof(PanelWs)) == cudaSuccess &&
             cudaMalloc(&h->lu_state, sizeof(LuState)) == cudaSuccess &&
             cudaMalloc(&h->piv_local, kMaxPiv * sizeof(int)) == cudaSuccess &&
@@ -85,7 +85,7 @@ extern "C" int mla_create(int device, mla_handle* out) {
             cudaMalloc(&h->widths_dev, kWidthsCap * sizeof(int32_t)) == cudaSuccess &&
             cudaMalloc(&h->resid_dev, 4 * sizeof(double)) == cudaSuccess;
   if (!ok) { mla_destroy(h); return MLA_E_NOMEM; }
-  cudaMemset(h->plan, 0, sizeof(PivPlan));
+  cudaMemset(h->plan, 0, 2 * sizeof(PivPlan));
   cudaMemset(h->panel_ws, 0, sizeof(PanelWs));
   cudaMemset(h->lu_state, 0, sizeof(LuState));
   h->apply_tag = 0x40000000u;   // far above any iteration number the persistent kernel tags flags with

@@ -133,7 +133,7 @@ __device__ inline void item_prep(const GetrfArgs& a, const IterShape& s, int c0,
   // given them the interchanges AND their A12 rows
   int lo = imax(c0, s.pend);
   if (lo < c0 + cw) {
-    laswp_apply_cols(a.A + (int64_t)lo * a.ld + s.q0, a.ld, c0 + cw - lo, a.plan->ref(), smem, kLaswpBufDoubles);
+    laswp_apply_cols(a.A + (int64_t)lo * a.ld + s.q0, a.ld, c0 + cw - lo, (a.plan + (s.it & 1))->ref(), smem, kLaswpBufDoubles);
     trsm_strip(a.A + (int64_t)s.q0 * a.ld + s.q0, s.kk, a.ld, a.A + (int64_t)lo * a.ld + s.q0, c0 + cw - lo, a.ld, smem);
   }
   __syncthreads();
@@ -333,7 +333,7 @@ __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* 
       item_prep(a, s, c0, imin(TRSM_CW, a.n - c0), &st->rprep_done[it.strip], smem);
     } else if (it.kind == 4) {
       const int c0 = it.strip * LEFT_CW;
-      laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), a.plan->ref(), smem,
+      laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), (a.plan + (s.it & 1))->ref(), smem,
                        kLaswpBufDoubles);
     }
     if (dbgc2 && it.kind != 0) {
@@ -370,6 +370,20 @@ __device__ inline int run_rq(const GetrfArgs& a, const IterShape& s, double* sme
 }
 
 // The persistent kernel body.  Cooperative launch, one CTA per SM.
+// Global pivots (lu.py:236,317: panel-local -> global) and the interchange plan of a factored panel
+// that starts at row/column q.  Collective over the CTA; kept out of line so that the persistent
+// kernel's tile loops do not depend on it.
+__device__ __noinline__ void publish_pivots(int* ipiv, const int* piv_local, int q, int k_new, int rows,
+                                            PivPlan* plan, double* smem) {
+  const int tid = threadIdx.x;
+  for (int t = tid; t < k_new; t += kThreads) ipiv[q + t] = q + piv_local[t];
+  if (tid < 32) {
+    int* scratch = reinterpret_cast<int*>(smem);
+    build_pivot_plan(piv_local, k_new, (int64_t)rows, false, plan->ref(), scratch, scratch + kMaxPiv,
+                     scratch + 3 * kMaxPiv, 2 * kMaxPiv, scratch + 5 * kMaxPiv);
+  }
+}
+
 __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int smem_doubles) {
   LuState* st = a.st;
   const int G = gridDim.x, bid = blockIdx.x, tid = threadIdx.x;
@@ -395,6 +409,10 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
   int singular = pr.singular, et_events = 0, n_panels = 0, ws_joins = 0;
   int q0 = 0, q1 = 0;
 
+  // The interchange plan is double-buffered by iteration parity: iteration `it` applies plan[it & 1]
+  // while the panel lead may already be writing plan[(it + 1) & 1].
+  int it_next = 1;
+  bool prebuilt = false;
   const bool dbgk = (bid == G - 1) && tid == 0;
   if (tid < 8) g_dbg[tid] = 0ull;
   __syncthreads();
@@ -406,11 +424,10 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
     all.barrier();
     if (!all.ok) break;
     if (bid == 0) {
-      for (int t = tid; t < k_new; t += kThreads) a.ipiv[q1_of_panel + t] = q1_of_panel + a.piv_local[t];
-      if (tid < 32) {
-        int* scratch = reinterpret_cast<int*>(smem);
-        build_pivot_plan(a.piv_local, k_new, (int64_t)(m - q1_of_panel), false, a.plan->ref(), scratch,
-                         scratch + kMaxPiv, scratch + 3 * kMaxPiv, 2 * kMaxPiv, scratch + 5 * kMaxPiv);
+      // global pivots + interchange plan of the just-factored panel, unless the panel team's lead
+      // already produced them right after its panel (look-ahead variants)
+      if (!prebuilt) {
+        publish_pivots(a.ipiv, a.piv_local, q1_of_panel, k_new, m - q1_of_panel, a.plan + (it_next & 1), smem);
       }
       if (tid == 0) {
         if (a.widths && n_panels < a.widths_cap) a.widths[n_panels] = k_new;
@@ -433,12 +450,14 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
     all.barrier();
     if (dbgk) g_dbg[5] += globaltimer_ns() - b_t0;
     if (!all.ok) break;
+    prebuilt = false;
+    ++it_next;
     IterShape s = iter_shape(st, m, n, G);
     if (*((volatile const int*)&st->done)) {
       // ---- final_sync (lu.py:328-332): last panel's interchanges for the columns to its left ------
       for (int l = bid; l < s.nleft; l += G) {
         int c0 = l * LEFT_CW;
-        laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), a.plan->ref(), smem,
+        laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), (a.plan + (s.it & 1))->ref(), smem,
                          kLaswpBufDoubles);
       }
       break;
@@ -474,6 +493,13 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
             st->trace[s.it - 1][2] = globaltimer_ns();
             st->trace[s.it - 1][4] = ((unsigned long long)s.w << 32) | (unsigned)pr.cols_factored;
           }
+        }
+        if (bid == 0 && pf.ok) {
+          // off the critical path of the update: the next iteration's pivots and plan
+          __syncthreads();
+          publish_pivots(a.ipiv, a.piv_local, s.q1, pr.cols_factored, m - s.q1, a.plan + ((s.it + 1) & 1), smem);
+          __syncthreads();
+          prebuilt = true;
         }
         if (ws && pf.ok) {
           // worker sharing: the quiesced panel team joins the update queue (pool.py:377-414)

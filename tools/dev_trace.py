@@ -33,5 +33,10 @@ for i in range(len(t)):
     tot["pq"] += row[0]; tot["panel"] += row[1]; tot["rq"] += row[2]; tot["iter"] += row[3]
     if i < 6 or i % max(1, len(t) // 24) == 0 or i > len(t) - 4:
         print(f"{i+1:4d} {w:4d} {k:5d} {row[0]:7.0f} {row[1]:8.0f} {row[2]:7.0f} {row[3]:8.0f}")
+ub = [(int(t[i][3]) - int(t[i][0])) >= (int(t[i][2]) - int(t[i][0])) for i in range(len(t))]
+it_us = [((t[i + 1][0] if i + 1 < len(t) else max(t[i][2], t[i][3])) - t[i][0]) / 1e3 for i in range(len(t))]
+print("  update-bound iterations: %d, %.1f ms;  panel-bound iterations: %d, %.1f ms (of which panel+pq %.1f ms)" % (
+    sum(ub), sum(x for x, u in zip(it_us, ub) if u) / 1e3, len(ub) - sum(ub), sum(x for x, u in zip(it_us, ub) if not u) / 1e3,
+    sum((int(t[i][2]) - int(t[i][0])) / 1e3 for i in range(len(t)) if not ub[i]) / 1e3))
 print("  totals (ms):", {k: round(v / 1e3, 2) for k, v in tot.items()})
 print("  panel phases of all panels (ms): trsm %.2f gemm %.2f steps %.2f (xchg %.2f) wb+swap %.2f bar %.2f" % tuple(x / 1e6 / 2 for x in prof[:3] + prof[5:6] + prof[3:5]))
