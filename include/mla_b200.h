@@ -56,7 +56,8 @@ typedef struct {
   int32_t et_events;
   int32_t n_panels;         /* number of panels factored (prologue included)                  */
   int32_t ws_joins;         /* iterations in which panel SMs joined the update queue (WS)     */
-  int32_t reserved[3];
+  int32_t sm_pf_peak;       /* largest panel team used (== sm_pf unless mla_set_panel_sms_max)  */
+  int32_t reserved[2];
 } mla_lu_info;
 
 /* Workspace / lifetime.  mla_create binds to `device` (cudaSetDevice) and sizes the persistent
@@ -110,6 +111,15 @@ int mla_panel_ll(mla_handle h, double* P, int64_t m, int64_t w, int64_t ld, int3
 int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
                  int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
                  int32_t* widths, int widths_cap, void* stream);
+
+/* Malleable SM split for the following mla_getrf_la* calls on this handle.  0 (default) keeps the
+ * reference's behaviour: the panel team has sm_pf SMs in every iteration (the split is restored each
+ * iteration, lu.py:270-273; WS only lends panel SMs to the update inside an iteration).
+ * sm_pf_max > sm_pf additionally lets the panel team grow between iterations -- doubled, up to
+ * sm_pf_max, after an iteration whose panel finished after the remainder update, halved (not below
+ * sm_pf) after one whose panel took under a third of the iteration.  Pivots and factors do not depend
+ * on the split.  Returns MLA_E_INVALID for negative values. */
+int mla_set_panel_sms_max(mla_handle h, int sm_pf_max);
 
 /* Same, reading the info back (synchronises the stream). */
 int mla_getrf_la_sync(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv,

@@ -17,7 +17,7 @@ _i64, _i32, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
 
 class LuInfo(ctypes.Structure):
     _fields_ = [("cols_factored", _i32), ("singular", _i32), ("et_events", _i32),
-                ("n_panels", _i32), ("ws_joins", _i32), ("reserved", _i32 * 3)]
+                ("n_panels", _i32), ("ws_joins", _i32), ("sm_pf_peak", _i32), ("reserved", _i32 * 2)]
 
 
 _lib = None
@@ -60,6 +60,8 @@ def lib() -> ctypes.CDLL:
     L.mla_gemm_half_experiment.restype = ctypes.c_int
     L.mla_apply_panel.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp]
     L.mla_apply_panel.restype = ctypes.c_int
+    L.mla_set_panel_sms_max.argtypes = [_vp, ctypes.c_int]
+    L.mla_set_panel_sms_max.restype = ctypes.c_int
     L.mla_getrf_debug.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64)]
     L.mla_getrf_debug.restype = ctypes.c_int
     L.mla_panel_profile.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
@@ -75,7 +77,7 @@ def lib() -> ctypes.CDLL:
 EXPORTS = ("mla_version", "mla_create", "mla_destroy", "mla_num_sms", "mla_last_cuda_error",
            "mla_gemm", "mla_trsm_llu", "mla_laswp", "mla_panel_ll", "mla_getrf_la",
            "mla_getrf_la_sync", "mla_getrf_la_host", "mla_fill_random", "mla_panel_profile", "mla_getrf_trace", "mla_laswp_async", "mla_getrf_debug",
-           "mla_gemm_half_experiment", "mla_apply_panel")
+           "mla_gemm_half_experiment", "mla_apply_panel", "mla_set_panel_sms_max")
 
 
 class MlaError(RuntimeError):

@@ -35,6 +35,7 @@ struct mla_handle_s {
   int last_cuda;
   unsigned* ctrl;        // CW_COUNT words (device)
   unsigned* ctrl_host;   // pinned mirror
+  int sm_pf_max = 0;     // malleable panel team: upper size (0 = fixed split)
   PivPlan* plan;         // device: permutation plan of the last pivot block
   PanelWs* panel_ws;     // device: exchange slots of the panel team
   LuState* lu_state;     // device: persistent-kernel state
@@ -475,10 +476,16 @@ extern "C" int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64
   CK(h, cudaMemsetAsync(h->ctrl, 0, CW_COUNT * sizeof(unsigned), s));
   CK(h, cudaMemsetAsync(h->lu_state, 0, sizeof(LuState), s));
   GetrfArgs a{A, (int)m, (int)n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks < 1 ? 1 : q_chunks,
-              h->lu_state, h->plan, h->panel_ws, h->piv_local, h->ctrl, info_dev, widths, widths_cap};
+              h->sm_pf_max, h->lu_state, h->plan, h->panel_ws, h->piv_local, h->ctrl, info_dev, widths, widths_cap};
   void* args[] = {&a};
   int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
   CK(h, cudaLaunchCooperativeKernel((void*)k_getrf, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
+  return MLA_OK;
+}
+
+extern "C" int mla_set_panel_sms_max(mla_handle h, int sm_pf_max) {
+  if (!h || sm_pf_max < 0) return MLA_E_INVALID;
+  h->sm_pf_max = sm_pf_max;
   return MLA_OK;
 }
 

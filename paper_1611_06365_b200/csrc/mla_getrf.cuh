@@ -57,6 +57,9 @@ struct LuState {
   unsigned rprep_done[kMaxStrips];
   // outcome
   int singular, et_events, n_panels, ws_joins, panel_cols;
+  // malleable split: panel-team size of the current iteration and the stamps that drive it
+  int sm_pf_cur, sm_pf_peak;
+  unsigned long long t_panel_end, t_rq_done;
   // device trace (globaltimer ns), one row per outer iteration (first kTraceCap): [0] iteration
   // start, [1] PQ complete (panel may start), [2] panel end, [3] RQ complete, [4] width<<32|k_new
   unsigned long long trace[1024][5];
@@ -71,6 +74,7 @@ struct GetrfArgs {
   double* A; int m, n; int64_t ld;
   int* ipiv;                 // global pivots out (device int32[n])
   int b_outer, b_inner, variant, sm_pf, q_chunks;
+  int sm_pf_max;             // 0: fixed split; > sm_pf: the panel team may grow up to this many CTAs
   LuState* st;
   PivPlan* plan;             // plan of the previously factored panel (view rows start at q0)
   PanelWs* pws;
@@ -356,6 +360,7 @@ __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* 
     unsigned old = atom_add_release(done, (unsigned)executed);
     if (which && old + (unsigned)executed == (unsigned)total) {
       if (signal_ru_done) st_release(&st->ru_done, (unsigned)s.it);
+      st->t_rq_done = globaltimer_ns();
       if (s.it <= kTraceCap) st->trace[s.it - 1][3] = globaltimer_ns();
     }
   }
@@ -390,10 +395,18 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
   unsigned* abort_word = a.ctrl;  // CW_ABORT == 0
   Team all, pf;
   all.init(bid, G, a.ctrl + 2 /*CW_BAR_ALL*/, abort_word);
+  pf.init(bid, G, a.ctrl + 3 /*CW_BAR_PF*/, abort_word);   // re-formed at the start of every iteration
   const bool la = a.variant != MLA_VARIANT_LU && G >= 2;
-  const int sm_pf = la ? imax(1, imin(a.sm_pf, G - 1)) : G;
-  pf.init(bid, sm_pf, a.ctrl + 3 /*CW_BAR_PF*/, abort_word);
-  const bool is_pf = la && bid < sm_pf;
+  // Panel-team size.  Fixed at sm_pf (the reference's t_pf, restored every iteration, lu.py:270-273),
+  // or -- with sm_pf_max > sm_pf -- malleable between iterations: doubled after an iteration in which
+  // the panel finished after the remainder update (the panel was the critical path), halved again
+  // after one in which it took less than a third of the iteration.  The factors do not depend on
+  // the team size (pivot search and every row's dot products are the same for any split).
+  const int sm_pf_lo = la ? imax(1, imin(a.sm_pf, G - 1)) : G;
+  const int sm_pf_hi = la ? imax(sm_pf_lo, imin(a.sm_pf_max, G - 1)) : G;
+  int sm_pf = sm_pf_lo;
+  bool is_pf = la && bid < sm_pf;
+  unsigned long long t_iter0 = 0ull;
   const bool ws = la && (a.variant == MLA_VARIANT_LU_MB || a.variant == MLA_VARIANT_LU_ET ||
                          a.variant == MLA_VARIANT_LU_WS_STATIC);
   const bool et = la && a.variant == MLA_VARIANT_LU_ET;
@@ -444,6 +457,19 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
         st->it = st->it + 1;
         st->done = (q1 >= n) ? 1 : 0;
         st->pq_next = 0; st->pq_done = 0; st->rq_next = 0; st->rq_done = 0;
+        if (la) {
+          int T = sm_pf;
+          if (sm_pf_hi > sm_pf_lo && q1_of_panel > 0) {
+            const unsigned long long pe = *((volatile unsigned long long*)&st->t_panel_end);
+            const unsigned long long rd = *((volatile unsigned long long*)&st->t_rq_done);
+            if (rd == 0ull || pe > rd) T = imin(sm_pf_hi, 2 * T);
+            else if (3 * (pe - t_iter0) < (rd - t_iter0)) T = imax(sm_pf_lo, T / 2);
+          }
+          st->sm_pf_cur = T;
+          if (T > st->sm_pf_peak) st->sm_pf_peak = T;
+          st->t_rq_done = 0ull;
+          a.ctrl[3 /*CW_BAR_PF*/] = 0u;   // nobody is inside a panel-team barrier here
+        }
         st->singular = singular; st->et_events = et_events; st->n_panels = n_panels; st->ws_joins = ws_joins;
       }
     }
@@ -452,6 +478,12 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
     if (!all.ok) break;
     prebuilt = false;
     ++it_next;
+    if (la) {
+      sm_pf = *((volatile const int*)&st->sm_pf_cur);
+      is_pf = bid < sm_pf;
+      pf.init(bid, sm_pf, a.ctrl + 3 /*CW_BAR_PF*/, abort_word);
+      if (bid == 0 && tid == 0) t_iter0 = globaltimer_ns();
+    }
     IterShape s = iter_shape(st, m, n, G);
     if (*((volatile const int*)&st->done)) {
       // ---- final_sync (lu.py:328-332): last panel's interchanges for the columns to its left ------
@@ -489,6 +521,7 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
                       et ? &st->ru_done : nullptr, (unsigned)s.it, 0, a.pws, smem, smem_doubles, true);
         if (bid == 0 && tid == 0) {
           st_release(&st->pf_done, (unsigned)s.it);
+          st->t_panel_end = globaltimer_ns();
           if (tr) {
             st->trace[s.it - 1][2] = globaltimer_ns();
             st->trace[s.it - 1][4] = ((unsigned long long)s.w << 32) | (unsigned)pr.cols_factored;
@@ -538,6 +571,7 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
     a.info->et_events = st->et_events;
     a.info->n_panels = st->n_panels;
     a.info->ws_joins = st->ws_joins;
+    a.info->sm_pf_peak = st->sm_pf_peak;
   }
 }
 

@@ -34,6 +34,7 @@
 
 namespace mla {
 
+constexpr int kMinInner = 16;    // narrowest block the slab-fitting rule goes down to
 constexpr int kMaxInner = 128;   // widest block handled by the pivot-step kernel
 constexpr int kMaxTeam = 160;    // >= SM count
 
@@ -172,6 +173,13 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       int to_poll = b_inner - (j % b_inner);  // never straddle a poll position
       wb = imin(wb, to_poll);
     }
+    // ... and halved until every CTA's share of the block (rows x wb) fits its shared-memory slab:
+    // pivot steps on a resident slab cost a third of steps that stream the block through L2.
+    {
+      int rpc_max = (((m - j) + T - 1) / T + 31) & ~31;
+      int lds_max = ((rpc_max + 1) & ~1) + 2;
+      while (wb > kMinInner && lds_max * wb > slab_cap) wb = imax(kMinInner, ((wb >> 1) + 7) & ~7);
+    }
     // ---- 1. U block -------------------------------------------------------------------------
     if (j > 0 && !eager_u) {
       {
@@ -201,11 +209,18 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
     if (nrows > 0) {
       if (j > 0) {
         for (int rt = r0; rt < r1; rt += GemmPanelCfg::BM)
-          for (int ct = 0; ct < wb; ct += GemmPanelCfg::BN)
-            gemm_tile<GemmPanelCfg>(P + rt, ld, P + (int64_t)(j + ct) * ld, ld, j,
-                                    P + (int64_t)(j + ct) * ld + rt, ld,
-                                    Sb + (int64_t)ct * lds + (rt - r0), lds, r1 - rt, wb - ct, 1.0, -1.0,
-                                    ring);
+          for (int ct = 0; ct < wb; ct += GemmPanelCfg::BN) {
+            if (wb - ct <= GemmPanel16Cfg::BN)
+              gemm_tile<GemmPanel16Cfg>(P + rt, ld, P + (int64_t)(j + ct) * ld, ld, j,
+                                        P + (int64_t)(j + ct) * ld + rt, ld,
+                                        Sb + (int64_t)ct * lds + (rt - r0), lds, r1 - rt, wb - ct, 1.0, -1.0,
+                                        ring);
+            else
+              gemm_tile<GemmPanelCfg>(P + rt, ld, P + (int64_t)(j + ct) * ld, ld, j,
+                                      P + (int64_t)(j + ct) * ld + rt, ld,
+                                      Sb + (int64_t)ct * lds + (rt - r0), lds, r1 - rt, wb - ct, 1.0, -1.0,
+                                      ring);
+          }
       } else if (resident) {
         for (int x = tid; x < nrows * wb; x += kThreads) {
           int c = x / nrows, i = x - c * nrows;

@@ -24,7 +24,8 @@ from .pool import CompletionFlag, SmPool, default_pool
 class LuResult:
     """Outcome of a factorization; the factors live in the input matrix (reference lu.py:33-41).
     `widths` (extension) lists every panel's factored width in order, which makes an ET run
-    replayable on the CPU oracle; `ws_joins` counts iterations in which panel SMs joined the update."""
+    replayable on the CPU oracle; `ws_joins` counts iterations in which panel SMs joined the update;
+    `t_pf_peak` is the largest panel team an adaptive split (pool.t_pf_max) used."""
 
     ipiv: PivotVector
     cols_factored: int
@@ -33,6 +34,7 @@ class LuResult:
     et_widths: tuple = ()
     widths: tuple = ()
     ws_joins: int = 0
+    t_pf_peak: int = 0
 
 
 def _check_tall(a: torch.Tensor) -> tuple[int, int, int]:
@@ -138,7 +140,8 @@ def lu_la(a: torch.Tensor, policy: Policy, pool: SmPool | None = None, cfg=None)
                                               _stream(a)), pool.handle, "lu_la")
     w = tuple(int(x) for x in widths[:min(cap, int(info.n_panels))])
     return LuResult(PivotVector(dev_piv.cpu().numpy(), device=dev_piv), n, bool(info.singular),
-                    int(info.et_events), et_widths_from(w, n, b_o, b_i), w, int(info.ws_joins))
+                    int(info.et_events), et_widths_from(w, n, b_o, b_i), w, int(info.ws_joins),
+                    int(info.sm_pf_peak))
 
 
 def et_widths_from(widths, n: int, b_o: int, b_i: int) -> tuple:

@@ -3,7 +3,9 @@
 The reference's pool is a set of CPU threads dispatched as one or two teams; here the "workers" are
 the SMs of one B200 and the dispatch happens inside the persistent kernel, so the pool only owns the
 library handle (workspace, flags, queues) and the default split.  `t` is the number of SMs, `t_pf`
-the default size of the panel team.  CompletionFlag is a device word (pool.py:28-49).
+the default size of the panel team, `t_pf_max` how far the panel team may grow between iterations
+when the panel is the critical path (0 = fixed split, the reference's behaviour; the result does not
+depend on it).  CompletionFlag is a device word (pool.py:28-49).
 """
 from __future__ import annotations
 
@@ -17,7 +19,7 @@ from . import _capi
 class SmPool:
     """One per device.  Context manager like the reference's WorkerPool."""
 
-    def __init__(self, device: int | None = None, t_pf: int = 16) -> None:
+    def __init__(self, device: int | None = None, t_pf: int = 16, t_pf_max: int | None = None) -> None:
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1611_06365_b200 needs a CUDA device; there is no CPU fallback")
         self.device = torch.cuda.current_device() if device is None else int(device)
@@ -25,7 +27,23 @@ class SmPool:
         _capi.check(_capi.lib().mla_create(self.device, ctypes.byref(self._h)), None, "mla_create")
         self.t = int(_capi.lib().mla_num_sms(self._h))
         self.t_pf = max(1, min(int(t_pf), self.t - 1))
+        # default: the panel team may take all but an eighth of the SMs once the panel is the critical path
+        self._t_pf_max = None
         self._closed = False
+        self.t_pf_max = self.t - max(1, self.t // 8) if t_pf_max is None else t_pf_max
+
+    @property
+    def t_pf_max(self) -> int:
+        return self._t_pf_max
+
+    @t_pf_max.setter
+    def t_pf_max(self, value: int) -> None:
+        value = int(value)
+        if value < 0:
+            raise ValueError("t_pf_max must be >= 0")
+        _capi.check(_capi.lib().mla_set_panel_sms_max(self.handle, min(value, self.t - 1)), self._h,
+                    "mla_set_panel_sms_max")
+        self._t_pf_max = min(value, self.t - 1)
 
     @property
     def handle(self):
