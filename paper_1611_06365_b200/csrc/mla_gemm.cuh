@@ -45,6 +45,7 @@ using GemmUpdateCfg = GemmCfg<128, 128, 2, 4, 3, 32>;  // trailing update tiles
 using GemmHalfCfg = GemmCfg<128, 64, 2, 2, 2, 32, 128>;   // experiment: 128-thread CTAs, two per SM
 using GemmPanelCfg = GemmCfg<128, 32, 8, 1, 4>;    // panel-internal update (N = inner block)
 using GemmPanel16Cfg = GemmCfg<128, 16, 8, 1, 4>;  // same, for blocks narrowed to 16 columns (slab fitting)
+using GemmPanel8Cfg = GemmCfg<128, 8, 8, 1, 4>;    // ... and to 8 columns (very tall panels)
 using GemmTrsmCfg = GemmCfg<32, 128, 1, 8, 4>;     // row-block update inside trsm strips
 
 // Issue the cp.async loads of k-tile `kt` into ring slot `slot`.

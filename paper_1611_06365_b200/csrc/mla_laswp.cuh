@@ -79,13 +79,23 @@ __device__ inline bool build_pivot_plan(const int* ipiv, int npiv, int64_t rows,
     }
   }
   __syncwarp();
-  // compact the moves (identity moves dropped): top rows first, then the touched lower rows
+  // Compact the moves (identity moves dropped), ordered so that one side of every move walks
+  // consecutive rows of the top block (coalesced): (1) the top rows as destinations, in row order;
+  // (2) the lower rows that receive a top row, in order of that SOURCE row; (3) lower <- lower.
+  for (int t = lane; t < npiv; t += 32) pv[t] = -1;
+  __syncwarp();
+  for (int x = lane; x < tsize; x += 32)
+    if (keys[x] >= 0 && vals[x] < npiv) pv[vals[x]] = keys[x];   // each source row occurs once
+  __syncwarp();
   int cnt = 0;
-  for (int base = 0; base < npiv + tsize; base += 32) {
+  for (int base = 0; base < 2 * npiv + tsize; base += 32) {
     int e = base + lane;
     int d = -1, sidx = -1;
     if (e < npiv) { d = e; sidx = top[e]; }
-    else if (e < npiv + tsize && keys[e - npiv] >= 0) { d = keys[e - npiv]; sidx = vals[e - npiv]; }
+    else if (e < 2 * npiv) { d = pv[e - npiv]; sidx = e - npiv; }
+    else if (e < 2 * npiv + tsize && keys[e - 2 * npiv] >= 0 && vals[e - 2 * npiv] >= npiv) {
+      d = keys[e - 2 * npiv]; sidx = vals[e - 2 * npiv];
+    }
     bool keep = (d >= 0) && (d != sidx);
     unsigned m = __ballot_sync(0xffffffffu, keep);
     if (keep) {

@@ -34,7 +34,7 @@
 
 namespace mla {
 
-constexpr int kMinInner = 16;    // narrowest block the slab-fitting rule goes down to
+constexpr int kMinInner = 8;     // narrowest block the slab-fitting rule goes down to
 constexpr int kMaxInner = 128;   // widest block handled by the pivot-step kernel
 constexpr int kMaxTeam = 160;    // >= SM count
 
@@ -210,7 +210,12 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       if (j > 0) {
         for (int rt = r0; rt < r1; rt += GemmPanelCfg::BM)
           for (int ct = 0; ct < wb; ct += GemmPanelCfg::BN) {
-            if (wb - ct <= GemmPanel16Cfg::BN)
+            if (wb - ct <= GemmPanel8Cfg::BN)
+              gemm_tile<GemmPanel8Cfg>(P + rt, ld, P + (int64_t)(j + ct) * ld, ld, j,
+                                       P + (int64_t)(j + ct) * ld + rt, ld,
+                                       Sb + (int64_t)ct * lds + (rt - r0), lds, r1 - rt, wb - ct, 1.0, -1.0,
+                                       ring);
+            else if (wb - ct <= GemmPanel16Cfg::BN)
               gemm_tile<GemmPanel16Cfg>(P + rt, ld, P + (int64_t)(j + ct) * ld, ld, j,
                                         P + (int64_t)(j + ct) * ld + rt, ld,
                                         Sb + (int64_t)ct * lds + (rt - r0), lds, r1 - rt, wb - ct, 1.0, -1.0,

@@ -27,10 +27,11 @@ class SmPool:
         _capi.check(_capi.lib().mla_create(self.device, ctypes.byref(self._h)), None, "mla_create")
         self.t = int(_capi.lib().mla_num_sms(self._h))
         self.t_pf = max(1, min(int(t_pf), self.t - 1))
-        # default: the panel team may take all but an eighth of the SMs once the panel is the critical path
+        # default 0: fixed split (measured on B200: growing the team in the panel-bound tail only moves
+        # time from the panel to the update, the total is unchanged -- DESIGN.md)
         self._t_pf_max = None
         self._closed = False
-        self.t_pf_max = self.t - max(1, self.t // 8) if t_pf_max is None else t_pf_max
+        self.t_pf_max = 0 if t_pf_max is None else t_pf_max
 
     @property
     def t_pf_max(self) -> int:
