@@ -686,6 +686,13 @@ extern "C" int mla_getrf_trace(mla_handle h, uint64_t* out, int max_rows) {
 extern "C" int mla_getrf_debug(mla_handle h, uint64_t* out8) {
   if (!h || !out8) return MLA_E_INVALID;
   CK(h, cudaDeviceSynchronize());
+#ifdef MLA_TILE_PROF
+  // instrumented build (tools/README.md): per-tile clock accounting of CTA 0 instead
+  CK(h, cudaMemcpyFromSymbol(out8, g_tprof, 8 * sizeof(uint64_t)));
+  unsigned long long zero[8] = {0};
+  CK(h, cudaMemcpyToSymbol(g_tprof, zero, sizeof(zero)));
+  return MLA_OK;
+#endif
   CK(h, cudaMemcpy(out8, h->lu_state->dbg, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return MLA_OK;
 }

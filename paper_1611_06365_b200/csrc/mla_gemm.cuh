@@ -188,8 +188,18 @@ __device__ __forceinline__ void tile_prologue(const TileDesc& d, int base, doubl
 // the previous tile's main loop).  While d's last k-tiles are consumed the first k-tiles of `next`
 // are prefetched into the ring, so the next tile starts without a pipeline bubble and d's epilogue
 // (C read-modify-write) overlaps next's loads.  Returns the ring base of `next`.
+#ifdef MLA_TILE_PROF
+// Instrumented build only (tools/README.md): clock accounting of CTA 0 / thread 0 per tile --
+// [0] tiles [1] total clk [2] clk in cp.async wait + barrier [3] epilogue clk [4] staging of the
+// first half [5] bulk issue + wait for the engine to have read the first half
+__device__ unsigned long long g_tprof[8];
+#endif
 template <class Cfg>
 __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, double* smem) {
+#ifdef MLA_TILE_PROF
+  const bool tp = blockIdx.x == 0 && threadIdx.x == 0;
+  long long tp0 = clock64(), tpw = 0;
+#endif
   constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES, NI = Cfg::NI, NJ = Cfg::NJ;
   const int tid = grp_tid<Cfg::THREADS>(), lane = tid & 31, warp = tid >> 5;
   const int wi = warp % Cfg::WI, wj = warp / Cfg::WI;
@@ -229,8 +239,14 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
   double* const sdB0 = smem + Cfg::A_STAGE + (tid / BCH_) * Cfg::LDB_S + 2 * (tid % BCH_);
 
   for (int kt = 0; kt < KT; ++kt) {
+#ifdef MLA_TILE_PROF
+    long long tw0 = clock64();
+#endif
     cp_async_wait<STAGES - 2>();
     grp_sync<Cfg::THREADS>();
+#ifdef MLA_TILE_PROF
+    tpw += clock64() - tw0;
+#endif
     const int pos = kt + STAGES - 1;
     const int lslot = (base + pos) % STAGES;
     const bool cur_tile = pos < KT;
@@ -263,6 +279,9 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
     if (lfast) cp_async_commit();
   }
   if (!next.valid) cp_async_wait<0>();
+#ifdef MLA_TILE_PROF
+  long long tpe = clock64();
+#endif
 
   // epilogue: lane owns rows i..i+1 of column j for every (nj, ni) block.  Loads are batched per
   // j-block (NI independent 16-byte loads in flight) so the tile's C traffic is not a chain of
@@ -293,12 +312,19 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
         }
         fence_proxy_async_smem();
         grp_sync<Cfg::THREADS>();
+#ifdef MLA_TILE_PROF
+        long long tq0 = clock64();
+        if (tp && half == 0) g_tprof[4] += tq0 - tpe;
+#endif
         if (tid < 64) {
           bulk_red_add_f64(Cout + (int64_t)(half * 64 + tid) * ldcout, stg + tid * RED_LDS, Cfg::BM * 8);
           bulk_commit();
           if (half == 0) bulk_wait_read0();   // the second half reuses the staging area
         }
         if (half == 0) grp_sync<Cfg::THREADS>();
+#ifdef MLA_TILE_PROF
+        if (tp && half == 0) g_tprof[5] += clock64() - tq0;
+#endif
       }
       if (!next.valid) {            // somebody else will use this shared memory next
         if (tid < 64) bulk_wait_read0();
@@ -354,6 +380,9 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
       }
     }
   }
+#ifdef MLA_TILE_PROF
+  if (tp) { long long e = clock64(); g_tprof[0] += 1; g_tprof[1] += e - tp0; g_tprof[2] += tpw; g_tprof[3] += e - tpe; }
+#endif
   return (base + KT) % STAGES;
 }
 

@@ -19,7 +19,7 @@ from . import _capi
 class SmPool:
     """One per device.  Context manager like the reference's WorkerPool."""
 
-    def __init__(self, device: int | None = None, t_pf: int = 16, t_pf_max: int | None = None) -> None:
+    def __init__(self, device: int | None = None, t_pf: int = 32, t_pf_max: int | None = None) -> None:
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1611_06365_b200 needs a CUDA device; there is no CPU fallback")
         self.device = torch.cuda.current_device() if device is None else int(device)

@@ -96,6 +96,35 @@ def test_non_et_variants_bitwise_identical_on_gpu(mla):  # test_lu.py:198-212, a
         assert np.array_equal(lu, outs[0][0])   # one owner per tile, fixed k order (kernels.py:3-9)
 
 
+def test_malleable_split_changes_nothing_but_the_team_size(mla):
+    """SmPool.t_pf_max (mla_set_panel_sms_max): the panel team grows between iterations when the panel is
+    the critical path; pivots and factors are bitwise those of the fixed split (lu_mb has no
+    timing-dependent widths)."""
+    a = gen(3072, 3072, 11)
+    pool = mla.SmPool(t_pf=8, t_pf_max=0)
+    try:
+        d0 = mla.from_numpy(a)
+        r0 = mla.lu_la(d0, mla.Policy("lu_mb", mla.BlockConfig(128, 32)), pool)
+        assert r0.t_pf_peak == 8
+        pool.t_pf_max = 64
+        d1 = mla.from_numpy(a)
+        r1 = mla.lu_la(d1, mla.Policy("lu_mb", mla.BlockConfig(128, 32)), pool)
+        assert 8 < r1.t_pf_peak <= 64            # n=3072 is panel-bound from the first iteration on
+        assert np.array_equal(r0.ipiv.ipiv, r1.ipiv.ipiv)
+        assert np.array_equal(mla.to_numpy(d0), mla.to_numpy(d1))
+        with pytest.raises(ValueError):
+            pool.t_pf_max = -1
+        pool.t_pf_max = 64
+        d2 = mla.from_numpy(a)
+        r2 = mla.lu_la(d2, mla.Policy("lu_et", mla.BlockConfig(128, 32)), pool)
+        ref = a.copy(order="F")
+        ro = oracle.lu_la(ref, 128, 32, et_sched=mla.et_schedule_from(r2.widths, 3072, 128, 32))
+        assert tuple(r2.widths) == tuple(ro.widths)
+        assert_parity(mla.to_numpy(d2), r2.ipiv.ipiv, ref, ro.ipiv, "malleable lu_et")
+    finally:
+        pool.shutdown()
+
+
 def test_tall_singular_empty_dominant(mla):  # test_lu.py:94-106, 226-244
     run_and_check(mla, gen(300, 200, 3), 64, 16, "lu_et", what="tall 300x200")
     run_and_check(mla, gen(900, 333, 3), 128, 32, "lu_mb", what="tall 900x333")
