@@ -98,8 +98,7 @@ struct PanelResult {
 };
 
 struct PanelShared {
-  double u[kMaxInner];           // pivot row (winner's values)
-  double d[kMaxInner];           // old diagonal row
+  double u2[2][kMaxInner];       // pivot row (winner's values) of the current / the previous step
   double red_val[8];
   int red_row[8];
   int piv[kMaxInner];            // block pivots, panel-local rows
@@ -245,21 +244,64 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       double v = fabs(Sb[i - r0]);
       if (cand_better(v, i, cv, cr)) { cv = v; cr = i; }
     }
+    // Look-ahead of the exchange over the update (slab in shared memory): a step's rank-1 update is
+    // split into F1 = scale + column c+1 (which yields the next candidates) and F2 = columns c+2.. ;
+    // F2 of step c-1 runs on warps 1-7 WHILE warp 0 runs the exchange of step c.  The two rows that
+    // exchange publishes / interchanges (the local candidate row and the diagonal row) are brought up
+    // to date by warp 0 itself and skipped by F2, so the two never touch the same entries.
+    const bool la_steps = resident;
+    int f2_c = -1;                     // step whose columns f2_c+2.. still await their update
     for (int c = 0; c < wb; ++c) {
       const int jc = j + c;            // diagonal row / global column of this step
       ++seq;
-      // A: per-warp candidates -> shared memory
+      double* const ucur = sh.u2[c & 1];
+      const double* const uprev = sh.u2[(c & 1) ^ 1];
+      // A: per-warp candidates -> shared memory; every warp then knows the CTA's candidate row
       cand_warp_reduce(cv, cr);
       if (lane == 0) { sh.red_val[warp] = cv; sh.red_row[warp] = cr; }
       __syncthreads();
-      // B-E: warp 0 runs the whole exchange while the other warps wait at the next barrier
+      double bv = (lane < 8) ? sh.red_val[lane] : -2.0;
+      int br = (lane < 8) ? sh.red_row[lane] : 0x7fffffff;
+      cand_warp_reduce(bv, br);
+      const bool have = bv >= 0.0;
+      const bool own_diag = (jc >= r0 && jc < r1);
+      if (warp != 0 && f2_c >= 0) {
+        // F2 of the previous step on every row except warp 0's two
+        const int64_t lcol = (int64_t)f2_c * lds;
+        for (int i = imax(r0, jc) + (tid - 32); i < r1; i += kThreads - 32) {
+          if (i == jc || (have && i == br)) continue;
+          double* __restrict__ row = Sb + (i - r0);
+          const double l = row[lcol];
+          for (int cb = f2_c + 2; cb < wb; cb += 8) {
+            double x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = (cb + e < wb) ? row[(int64_t)(cb + e) * lds] : 0.0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) if (cb + e < wb) x[e] = fma(-l, uprev[cb + e], x[e]);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) if (cb + e < wb) row[(int64_t)(cb + e) * lds] = x[e];
+          }
+        }
+      }
+      // B-E: warp 0 runs the whole exchange
       if (warp == 0) {
         unsigned long long xt0 = (rank == 0 && lane == 0) ? globaltimer_ns() : 0ull;
-        double bv = (lane < 8) ? sh.red_val[lane] : -2.0;
-        int br = (lane < 8) ? sh.red_row[lane] : 0x7fffffff;
-        cand_warp_reduce(bv, br);
-        const bool have = bv >= 0.0;
-        const bool own_diag = (jc >= r0 && jc < r1);
+        if (f2_c >= 0) {
+          const int64_t lcol = (int64_t)f2_c * lds;
+          const bool two = own_diag && !(have && br == jc);
+          for (int cc = f2_c + 2 + lane; cc < wb; cc += 32) {
+            const double uc = uprev[cc];
+            if (have) {
+              double* e = Sb + (int64_t)cc * lds + (br - r0);
+              *e = fma(-Sb[lcol + (br - r0)], uc, *e);
+            }
+            if (two) {
+              double* e = Sb + (int64_t)cc * lds + (jc - r0);
+              *e = fma(-Sb[lcol + (jc - r0)], uc, *e);
+            }
+          }
+          __syncwarp();
+        }
         bool good = true;
         double wv;
         int p;
@@ -270,7 +312,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
           if (wv > 0.0) {
             for (int cc = lane; cc < wb; cc += 32) {
               double uu = Sb[(int64_t)cc * lds + (p - r0)];
-              sh.u[cc] = uu;
+              ucur[cc] = uu;
               if (p != jc) {
                 double dd = Sb[(int64_t)cc * lds + (jc - r0)];
                 Sb[(int64_t)cc * lds + (jc - r0)] = uu;
@@ -334,7 +376,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
               }
               if ((unsigned)hi != seq && !poll_unit(&slots[wrank].rv[cc], seq, team.abort_word, lo, hi)) { good = false; break; }
               double uu = __longlong_as_double((long long)lo);
-              sh.u[cc] = uu;
+              ucur[cc] = uu;
               if (p != jc) {
                 unsigned long long lo2 = dlo, hi2 = dhi;
                 if (cc >= 32) ld_b128(&slots[drank].dg[cc], lo2, hi2);
@@ -357,6 +399,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       }
       __syncthreads();
       if (sh.flag) { team.ok = false; res.cols_factored = j; return res; }
+      f2_c = -1;
       const double wval = sh.win_val;
       if (!(wval > 0.0)) {
         // zero pivot column: record, flag, skip (lu.py:56-59); candidate of the next column fresh
@@ -372,10 +415,25 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       // F: scale + rank-1 update of rows below the diagonal, search next column's maximum.
       // Columns are processed in register chunks of 8 so the shared-memory loads of a row are in
       // flight together instead of forming a load->fma->store chain per column.
-      const double pivot = sh.u[c];
+      const double pivot = ucur[c];
       const double rinv = 1.0 / pivot;
       cv = -1.0; cr = 0x7fffffff;
-      if (resident) {
+      if (la_steps) {
+        // F1 only; the other columns follow during the next exchange (F2 above)
+        const double un = (c + 1 < wb) ? ucur[c + 1] : 0.0;
+        for (int i = imax(r0, jc + 1) + tid; i < r1; i += kThreads) {
+          double* __restrict__ row = Sb + (i - r0);
+          const double l = div_by_pivot(row[(int64_t)c * lds], pivot, rinv);
+          row[(int64_t)c * lds] = l;
+          if (c + 1 < wb) {
+            const double x = fma(-l, un, row[(int64_t)(c + 1) * lds]);
+            row[(int64_t)(c + 1) * lds] = x;
+            const double v = fabs(x);
+            if (cand_better(v, i, cv, cr)) { cv = v; cr = i; }
+          }
+        }
+        if (c + 2 < wb) f2_c = c;
+      } else if (resident) {
         for (int i = imax(r0, jc + 1) + tid; i < r1; i += kThreads) {
           double* __restrict__ row = Sb + (i - r0);
           const double l = div_by_pivot(row[(int64_t)c * lds], pivot, rinv);
@@ -385,7 +443,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
 #pragma unroll
             for (int e = 0; e < 8; ++e) x[e] = (cb + e < wb) ? row[(int64_t)(cb + e) * lds] : 0.0;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) if (cb + e < wb) x[e] = fma(-l, sh.u[cb + e], x[e]);
+            for (int e = 0; e < 8; ++e) if (cb + e < wb) x[e] = fma(-l, ucur[cb + e], x[e]);
 #pragma unroll
             for (int e = 0; e < 8; ++e) if (cb + e < wb) row[(int64_t)(cb + e) * lds] = x[e];
             if (cb == c + 1) {
@@ -424,9 +482,9 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
               if (i < r1) {
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
-                  if (cb + e < wb) row[r][(int64_t)(cb + e) * lds] = fma(-l[r], sh.u[cb + e], x[r][e]);
+                  if (cb + e < wb) row[r][(int64_t)(cb + e) * lds] = fma(-l[r], ucur[cb + e], x[r][e]);
                 if (cb == c + 1) {
-                  double v = fabs(fma(-l[r], sh.u[cb], x[r][0]));
+                  double v = fabs(fma(-l[r], ucur[cb], x[r][0]));
                   if (cand_better(v, i, cv, cr)) { cv = v; cr = i; }
                 }
               }
