@@ -199,7 +199,9 @@ def test_panel_golden(mla, golden, c):
 
 
 @pytest.mark.parametrize("m,w,b,team", [(64, 48, 8, 1), (200, 96, 32, 3), (2048, 256, 32, 16), (5000, 256, 32, 8),
-                                        (40000, 128, 32, 16), (1000, 192, 64, 148), (3000, 96, 96, 7), (777, 130, 16, 5)])
+                                        (40000, 128, 32, 16), (1000, 192, 64, 148), (3000, 96, 96, 7), (777, 130, 16, 5),
+                                        # slab fitting: 2000 rows per CTA -> 8-column device blocks; 1000 -> 16
+                                        (4000, 64, 32, 2), (16000, 128, 64, 16)])
 def test_panel_vs_oracle(mla, m, w, b, team):  # test_lu.py:121-129 (same pivots), any team size
     a = gen(m, w, 5)
     d = mla.from_numpy(a)
