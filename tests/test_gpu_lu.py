@@ -125,6 +125,26 @@ def test_malleable_split_changes_nothing_but_the_team_size(mla):
         pool.shutdown()
 
 
+@pytest.mark.parametrize("n,b_o,b_i,t_pf,reps", [(3072, 256, 32, 12, 12), (9000, 512, 64, 6, 4), (2048, 128, 16, 40, 12)])
+def test_repeated_runs_are_bitwise_identical(mla, n, b_o, b_i, t_pf, reps):
+    """Race detector of last resort (no sanitizer on the pool): lu_mb has a fixed width schedule, one owner
+    per tile and per slab row, so ANY run-to-run difference is a data race (tile reductions vs readers,
+    pivot-step look-ahead vs the exchange, plan double buffering).  9000/6 = 1500 rows per panel CTA
+    runs the 8-column device blocks."""
+    a = mla.alloc_matrix(n, n)
+    mla.fill_random(a, 21, 2.0, -1.0)
+    first = None
+    for _ in range(reps):
+        d = a.clone()
+        r = mla.lu_la(d, mla.Policy("lu_mb", mla.BlockConfig(b_o, b_i), t_pf=t_pf))
+        cur = (r.ipiv.ipiv.copy(), d.clone())
+        if first is None:
+            first = cur
+        else:
+            assert np.array_equal(first[0], cur[0])
+            assert bool((first[1] == cur[1]).all())
+
+
 def test_tall_singular_empty_dominant(mla):  # test_lu.py:94-106, 226-244
     run_and_check(mla, gen(300, 200, 3), 64, 16, "lu_et", what="tall 300x200")
     run_and_check(mla, gen(900, 333, 3), 128, 32, "lu_mb", what="tall 900x333")
