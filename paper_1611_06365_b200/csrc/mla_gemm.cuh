@@ -191,7 +191,8 @@ __device__ __forceinline__ void tile_prologue(const TileDesc& d, int base, doubl
 #ifdef MLA_TILE_PROF
 // Instrumented build only (tools/README.md): clock accounting of CTA 0 / thread 0 per tile --
 // [0] tiles [1] total clk [2] clk in cp.async wait + barrier [3] epilogue clk [4] staging of the
-// first half [5] bulk issue + wait for the engine to have read the first half
+// first half [5] bulk issue + wait for the engine to have read the first half [6] start-of-tile wait for the
+// previous tile's read + issue of the second half's operations [7] proxy fence of the second half
 __device__ unsigned long long g_tprof[8];
 #endif
 template <class Cfg>
@@ -226,7 +227,13 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
 
   // the previous tile's epilogue may still be reading its staged accumulators out of the ring slot this
   // tile's first load will overwrite
+#ifdef MLA_TILE_PROF
+  long long tr0 = clock64();
+#endif
   if constexpr (Cfg::FAST_OK) bulk_wait_read0();
+#ifdef MLA_TILE_PROF
+  if (tp) g_tprof[6] += clock64() - tr0;
+#endif
 
   // fast-path constants of this tile and of the prefetched successor, hoisted out of the k loop
   const FastSrc<Cfg> fd = make_fast_src<Cfg>(d);
@@ -310,15 +317,25 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
               *reinterpret_cast<double2*>(sp + b * 8) = make_double2(-acc[a][b][0], -acc[a][b][1]);
           }
         }
+#ifdef MLA_TILE_PROF
+        long long tf0 = clock64();
+#endif
         fence_proxy_async_smem();
+#ifdef MLA_TILE_PROF
+        long long tf1 = clock64();
+#endif
         grp_sync<Cfg::THREADS>();
 #ifdef MLA_TILE_PROF
         long long tq0 = clock64();
         if (tp && half == 0) g_tprof[4] += tq0 - tpe;
+        if (tp && half == 1) { g_tprof[7] += tf1 - tf0; }
 #endif
         if (tid < 64) {
           bulk_red_add_f64(Cout + (int64_t)(half * 64 + tid) * ldcout, stg + tid * RED_LDS, Cfg::BM * 8);
           bulk_commit();
+#ifdef MLA_TILE_PROF
+          if (tp && half == 1) g_tprof[6] += clock64() - tq0;   // (reuses slot 6) issue time of the second half
+#endif
           if (half == 0) bulk_wait_read0();   // the second half reuses the staging area
         }
         if (half == 0) grp_sync<Cfg::THREADS>();

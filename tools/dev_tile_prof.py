@@ -17,4 +17,4 @@ for m, k in [(2048, 512), (16384, 512), (32768, 512), (16384, 256)]:
     L.mla_getrf_debug(h, dbg)
     t = max(1, dbg[0])
     ideal = 128 * 128 * k * 2 / 512 * 16 / 4 / 2   # clk: DMMAs per SMSP * 16
-    print(f"m={m} k={k}: {2.0*m*m*k/ms*1e-9:.2f} TF; CTA0: {t} tiles, {dbg[1]/t:.0f} clk/tile, wait+sync {dbg[2]/t:.0f}, epilogue {dbg[3]/t:.0f} (stage half0 {dbg[4]/t:.0f}, issue+wait_read {dbg[5]/t:.0f})")
+    print(f"m={m} k={k}: {2.0*m*m*k/ms*1e-9:.2f} TF; CTA0: {t} tiles, {dbg[1]/t:.0f} clk/tile, wait+sync {dbg[2]/t:.0f}, epilogue {dbg[3]/t:.0f} (stage half0 {dbg[4]/t:.0f}, issue+wait_read {dbg[5]/t:.0f}; start wait + issue of half 1 {dbg[6]/t:.0f}, fence of half 1 {dbg[7]/t:.0f})")
