@@ -127,7 +127,10 @@ int mla_getrf_la_sync(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld,
                       mla_lu_info* info_host, int32_t* widths_host, int widths_cap, void* stream);
 
 /* End-to-end form with HOST buffers (what bench.py's `e2e` times): uploads A (m x n, ld_host),
- * factors on the device, downloads the packed factors and the pivots.  Synchronous. */
+ * factors on the device, downloads the packed factors and the pivots.  The download overlaps the
+ * factorization: rows above the current panel are final (every later interchange, solve and update
+ * touches lower rows only), the kernel reports that row through a mapped host word, and the finished
+ * row blocks are copied out on a second stream while the kernel is still running.  Synchronous. */
 int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_t ld_host,
                       int32_t* ipiv_host, int b_outer, int b_inner, int variant, int sm_pf,
                       int q_chunks, mla_lu_info* info_host);

@@ -3,7 +3,9 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -shared -Xcompiler -fPIC
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
+#include <thread>
 #include <new>
 
 #include "../../include/mla_b200.h"
@@ -43,6 +45,11 @@ struct mla_handle_s {
   mla_lu_info* info_dev; // device
   mla_lu_info* info_host;  // pinned
   int32_t* widths_dev;   // device, kWidthsCap
+  cudaStream_t s_main, s_copy;   // non-blocking streams of the _host entry point (factor / stream results out)
+  cudaEvent_t ev_done;
+  int* progress_host;    // pinned + mapped: number of leading rows that are final (written by the kernel)
+  int* progress_dev;     // device alias of progress_host
+  int* next_progress;    // consumed by the next mla_getrf_la launch (nullptr: no progress reports)
   double* a_dev;         // cached device matrix for the _host entry point
   size_t a_dev_bytes;
   int32_t* ipiv_dev;
@@ -85,6 +92,11 @@ extern "C" int mla_create(int device, mla_handle* out) {
             cudaMallocHost(&h->info_host, sizeof(mla_lu_info)) == cudaSuccess &&
             cudaMalloc(&h->widths_dev, kWidthsCap * sizeof(int32_t)) == cudaSuccess &&
             cudaMalloc(&h->resid_dev, 4 * sizeof(double)) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&h->s_main, cudaStreamNonBlocking) == cudaSuccess &&
+       cudaStreamCreateWithFlags(&h->s_copy, cudaStreamNonBlocking) == cudaSuccess &&
+       cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming) == cudaSuccess &&
+       cudaHostAlloc(&h->progress_host, 64, cudaHostAllocMapped) == cudaSuccess &&
+       cudaHostGetDevicePointer(&h->progress_dev, h->progress_host, 0) == cudaSuccess;
   if (!ok) { mla_destroy(h); return MLA_E_NOMEM; }
   cudaMemset(h->plan, 0, 2 * sizeof(PivPlan));
   cudaMemset(h->panel_ws, 0, sizeof(PanelWs));
@@ -108,6 +120,10 @@ extern "C" int mla_destroy(mla_handle h) {
   cudaFree(h->resid_dev);
   cudaFree(h->a_dev);
   cudaFree(h->ipiv_dev);
+  if (h->s_main) cudaStreamDestroy(h->s_main);
+  if (h->s_copy) cudaStreamDestroy(h->s_copy);
+  if (h->ev_done) cudaEventDestroy(h->ev_done);
+  if (h->progress_host) cudaFreeHost(h->progress_host);
   delete h;
   return MLA_OK;
 }
@@ -476,7 +492,8 @@ extern "C" int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64
   CK(h, cudaMemsetAsync(h->ctrl, 0, CW_COUNT * sizeof(unsigned), s));
   CK(h, cudaMemsetAsync(h->lu_state, 0, sizeof(LuState), s));
   GetrfArgs a{A, (int)m, (int)n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks < 1 ? 1 : q_chunks,
-              h->sm_pf_max, h->lu_state, h->plan, h->panel_ws, h->piv_local, h->ctrl, info_dev, widths, widths_cap};
+              h->sm_pf_max, h->next_progress, h->lu_state, h->plan, h->panel_ws, h->piv_local, h->ctrl, info_dev, widths, widths_cap};
+  h->next_progress = nullptr;
   void* args[] = {&a};
   int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
   CK(h, cudaLaunchCooperativeKernel((void*)k_getrf, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
@@ -527,16 +544,40 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
     CK(h, cudaMalloc(&h->ipiv_dev, (size_t)n * sizeof(int32_t)));
     h->ipiv_dev_n = (size_t)n;
   }
-  cudaStream_t s = 0;
+  // Upload, factor, and stream the result out WHILE the factorization runs: once an outer iteration
+  // has started with its panel at row q0, rows [0, q0) of the whole matrix are final (later
+  // interchanges, solves and updates only touch rows >= q0), so they are copied to the host as row
+  // blocks on a second stream.  The kernel reports q0 through a mapped host word.
+  cudaStream_t s = h->s_main;
+  *((volatile int*)h->progress_host) = 0;
   CK(h, cudaMemcpy2DAsync(h->a_dev, ld * sizeof(double), A_host, ld_host * sizeof(double), m * sizeof(double), n,
                           cudaMemcpyHostToDevice, s));
+  h->next_progress = h->progress_dev;
   int rc = mla_getrf_la(h, h->a_dev, m, n, ld, h->ipiv_dev, b_outer, b_inner, variant, sm_pf, q_chunks, h->info_dev,
                         nullptr, 0, s);
+  h->next_progress = nullptr;
   if (rc != MLA_OK) return rc;
-  CK(h, cudaMemcpy2DAsync(A_host, ld_host * sizeof(double), h->a_dev, ld * sizeof(double), m * sizeof(double), n,
-                          cudaMemcpyDeviceToHost, s));
-  CK(h, cudaMemcpyAsync(ipiv_host, h->ipiv_dev, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  CK(h, cudaMemcpyAsync(h->info_host, h->info_dev, sizeof(mla_lu_info), cudaMemcpyDeviceToHost, s));
+  CK(h, cudaEventRecord(h->ev_done, s));
+  const int64_t min_rows = 256;   // narrower row blocks make the strided copy inefficient
+  int64_t done_rows = 0;
+  while (true) {
+    cudaError_t q = cudaEventQuery(h->ev_done);
+    if (q != cudaSuccess && q != cudaErrorNotReady) { h->last_cuda = (int)q; return MLA_E_CUDA; }
+    const bool finished = (q == cudaSuccess);
+    int64_t ready = finished ? m : (int64_t)*((volatile int*)h->progress_host);
+    if (ready > m) ready = m;
+    if (ready - done_rows >= min_rows || (finished && ready > done_rows)) {
+      CK(h, cudaMemcpy2DAsync(A_host + done_rows, ld_host * sizeof(double), h->a_dev + done_rows, ld * sizeof(double),
+                              (size_t)(ready - done_rows) * sizeof(double), n, cudaMemcpyDeviceToHost, h->s_copy));
+      done_rows = ready;
+    } else if (!finished) {
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    if (finished && done_rows >= m) break;
+  }
+  CK(h, cudaMemcpyAsync(ipiv_host, h->ipiv_dev, n * sizeof(int32_t), cudaMemcpyDeviceToHost, h->s_copy));
+  CK(h, cudaMemcpyAsync(h->info_host, h->info_dev, sizeof(mla_lu_info), cudaMemcpyDeviceToHost, h->s_copy));
+  CK(h, cudaStreamSynchronize(h->s_copy));
   rc = check_abort(h, s);
   if (info_host) *info_host = *h->info_host;
   return rc;

@@ -75,6 +75,7 @@ struct GetrfArgs {
   int* ipiv;                 // global pivots out (device int32[n])
   int b_outer, b_inner, variant, sm_pf, q_chunks;
   int sm_pf_max;             // 0: fixed split; > sm_pf: the panel team may grow up to this many CTAs
+  int* progress;             // nullable, host-mapped: receives q0 = number of leading rows that are final
   LuState* st;
   PivPlan* plan;             // plan of the previously factored panel (view rows start at q0)
   PanelWs* pws;
@@ -451,6 +452,11 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
         q0 = q1_of_panel;
         q1 = q1_of_panel + k_new;
         st->q0 = q0; st->q1 = q1; st->pend = pend;
+        if (a.progress) {
+          // every write to rows < q0 precedes the grid barrier above; later work touches rows >= q0 only
+          __threadfence_system();
+          *((volatile int*)a.progress) = q0;
+        }
         st->w = imin(b_target, n - q1);
         st->b_target = b_target;
         st->npiv_prev = k_new;

@@ -145,6 +145,35 @@ def test_repeated_runs_are_bitwise_identical(mla, n, b_o, b_i, t_pf, reps):
             assert bool((first[1] == cur[1]).all())
 
 
+@pytest.mark.parametrize("m,n,pinned", [(200, 200, False), (3000, 3000, True), (5000, 3500, False), (6144, 6144, True)])
+def test_host_entry_streams_out_the_same_factors(mla, m, n, pinned):
+    """mla_getrf_la_host (what bench.py's e2e times): upload, factor, and copy finished row blocks to the
+    host while the factorization is still running.  lu_mb is deterministic, so the result must be
+    bitwise the device path's."""
+    import ctypes
+    import torch
+    from paper_1611_06365_b200 import _capi
+    pool = mla.default_pool()
+    a = gen(m, n, 17)                                   # column-major numpy
+    d = mla.from_numpy(a)
+    r = mla.lu_la(d, mla.Policy("lu_mb", mla.BlockConfig(256, 32)), pool)
+    want = mla.to_numpy(d)
+    pristine = torch.from_numpy(np.array(a.T, order="C", copy=True))   # (n, m): rows are the matrix's columns
+    host = torch.empty_like(pristine)
+    ipiv = torch.empty(n, dtype=torch.int32)
+    if pinned:
+        host, ipiv = host.pin_memory(), ipiv.pin_memory()
+    info = _capi.LuInfo()
+    for _ in range(2):                                  # second call reuses the cached device buffers
+        host.copy_(pristine)
+        rc = _capi.lib().mla_getrf_la_host(pool.handle, host.data_ptr(), m, n, m, ipiv.data_ptr(), 256, 32,
+                                           _capi.VARIANT_CODES["lu_mb"], pool.t_pf, 1, ctypes.byref(info))
+        _capi.check(rc, pool.handle, "mla_getrf_la_host")
+        assert np.array_equal(ipiv.numpy().astype(np.int64), r.ipiv.ipiv)
+        assert np.array_equal(host.numpy().T, want)
+        assert info.n_panels == len(r.widths)
+
+
 def test_tall_singular_empty_dominant(mla):  # test_lu.py:94-106, 226-244
     run_and_check(mla, gen(300, 200, 3), 64, 16, "lu_et", what="tall 300x200")
     run_and_check(mla, gen(900, 333, 3), 128, 32, "lu_mb", what="tall 900x333")
