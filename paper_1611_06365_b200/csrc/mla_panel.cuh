@@ -1,7 +1,8 @@
 // Panel factorization: left-looking blocked LU with partial pivoting, collective over a Team of
 // CTAs (reference lu.py:140-180 lu_blk_ll + lu.py:44-72 _unb_pivoted).
 //
-// Per inner block [j, j+wb) of the m x w panel (wb = b_inner):
+// Per device block [j, j+wb) of the m x w panel (wb = b_inner, halved down to 8 until a CTA's share of
+// the block fits its shared-memory slab; ET polls stay at multiples of b_inner):
 //   1. U block:  P[0:j, j:j+wb] = trilu(P[0:j,0:j])^-1 P[0:j, j:j+wb]  (lu.py:166) -- in the reference's
 //      left-looking order this is a trsm per block (stand-alone lu_blk_ll: columns dealt to the first
 //      CTAs); inside the persistent kernel (eager_u) it is already there, see 4b.
@@ -14,8 +15,9 @@
 //      wins ties, lu.py:53 -- and that row's wb values), the CTA owning the diagonal row publishes
 //      that row (16-byte self-validating words, no fences); after polling all slots every CTA knows
 //      the pivot row p, swaps its side of (j+c <-> p), forms the multipliers (lu.py:65-67) and applies
-//      the rank-1 update
-//      while already searching the next column's maximum.  An exactly-zero column records piv = j+c,
+//      the rank-1 update while already searching the next column's maximum.  With the slab in shared
+//      memory the update is split: column c+1 at once (it yields the next candidates), the remaining
+//      columns on warps 1-7 WHILE warp 0 already runs the next step's exchange.  An exactly-zero column records piv = j+c,
 //      raises the singular flag and is skipped (lu.py:56-59).
 //   4. the block's wb interchanges are applied to the other panel columns as one parallel
 //      permutation plan (equivalent data movement to lu.py:165,173-174,178; applying them eagerly
