@@ -425,8 +425,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_panel(PanelKArgs a) {
   extern __shared__ __align__(16) double smem[];
   Team team;
   team.init(blockIdx.x, gridDim.x, a.ctrl + CW_BAR_ALL, a.ctrl + CW_ABORT);
+  // Without a stop request nothing can observe the panel half-way, so the U rows are produced in Crout
+  // order (no chain of dependent solves per block); a stoppable panel keeps the reference's
+  // left-looking order: after a cut the untouched columns carry the interchanges and nothing else
+  // (lu.py:177-179, test_lu.py:132-145).
+  const bool stoppable = a.stop_flag != nullptr || a.stop_after_polls > 0;
   PanelResult r = panel_ll(team, a.P, a.m, a.w, a.ld, a.ipiv, a.b_inner, a.stop_flag, 0u, a.stop_after_polls,
-                           a.ws, smem, kDynSmemDoubles);
+                           a.ws, smem, kDynSmemDoubles, !stoppable);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.info->cols_factored = r.cols_factored;
     a.info->singular = r.singular;
