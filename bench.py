@@ -31,10 +31,10 @@ from paper_1611_06365_b200.workloads import CONFIGS, flops_lu, make_matrix  # no
 
 # DRAM bytes of ONE k_getrf launch on the default workload (n=32768, b=512/64, lu_et, sm_pf 32), from
 # `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` (profiles/r01_getrf_n32768_traffic.csv):
-# 493.9 GB read + 229.8 GB written; the algorithmic minimum (the trailing matrix read and written once
+# 493.3 GB read + 229.8 GB written; the algorithmic minimum (the trailing matrix read and written once
 # per iteration) is 2 * 8 * n^3 / (3 b) = 367 GB at b = 512 (ET cuts make the effective b smaller).
 # At b=256/32 the same measurement gave 577.2 + 423.0 GB against a minimum of 733 GB.
-DEFAULT_WORKLOAD_DRAM_BYTES = 493934044928 + 229825649152
+DEFAULT_WORKLOAD_DRAM_BYTES = 493252247808 + 229810838016
 
 FP64_TENSOR_PEAK_TFLOPS = 37.0   # measured on this pool's B200: tools/fp64_peak.cu (DMMA.8x8x4
                                  # issue-bound, 3 s sustained) -> profiles/r01_fp64_peak.log.
