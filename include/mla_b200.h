@@ -103,6 +103,12 @@ int mla_panel_ll(mla_handle h, double* P, int64_t m, int64_t w, int64_t ld, int3
                  const uint32_t* stop_flag, int stop_after_polls, int team_ctas, mla_lu_info* info,
                  void* stream);
 
+/* Asynchronous form for stream-ordered drivers (distributed.py): no stop flag, pivots stay on the
+ * device, nothing is read back; singular_accum (device int32, nullable) is OR-ed with the panel's
+ * singular flag. */
+int mla_panel_ll_async(mla_handle h, double* P, int64_t m, int64_t w, int64_t ld, int32_t* ipiv, int b_inner,
+                       int team_ctas, int32_t* singular_accum, void* stream);
+
 /* lu_la(a, policy, pool) -- lu.py:197-334.  Whole factorization P*A = L*U in place, one persistent
  * cooperative kernel: SM partition (sm_pf panel CTAs), atomic tile queue, WS and ET by device
  * flags.  ipiv: device int32[n], global 0-based.  widths (device int32[widths_cap], nullable)
@@ -142,6 +148,19 @@ int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_
  * (laswp -> trsm_llu -> gemm_malleable of lu.py:251-253, 280-281, 289, 306-308).  Asynchronous. */
 int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
                     int64_t cols, int64_t ldt, const int32_t* ipiv, void* stream);
+
+/* The two halves of mla_apply_panel.  prepare: interchange plan of the w pivots, empty work queue, fresh
+ * flag tag.  launch: `ctas` CTAs (0 = mla_set_update_sms / all) draining the prepared queue; a second
+ * launch of the same step on another stream JOINS that queue (worker sharing across kernels: the SMs that
+ * factored the next panel help with the update once the panel is done). */
+int mla_apply_panel_prepare(mla_handle h, const int32_t* ipiv, int64_t w, int64_t rows, void* stream);
+int mla_apply_panel_launch(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
+                           int64_t cols, int64_t ldt, int ctas, void* stream);
+
+/* Number of SMs mla_apply_panel launches on (0 = all).  A multi-GPU driver leaves a few SMs to the
+ * communication kernels, and the owner of the next panel runs that panel (mla_panel_ll_async, second
+ * handle, second stream) next to its update on the remaining SMs. */
+int mla_set_update_sms(mla_handle h, int ctas);
 
 /* fill_random(a, seed) -- matrix.py:44-63: SplitMix64 stream, bit-identical to the reference;
  * value = scale*u + shift with u in (0,1) (scale=1, shift=0 reproduces fill_random; 2,-1 gives the

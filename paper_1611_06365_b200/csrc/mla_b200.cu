@@ -38,6 +38,7 @@ struct mla_handle_s {
   unsigned* ctrl;        // CW_COUNT words (device)
   unsigned* ctrl_host;   // pinned mirror
   int sm_pf_max = 0;     // malleable panel team: upper size (0 = fixed split)
+  int update_sms = 0;    // grid of mla_apply_panel (0 = every SM)
   PivPlan* plan;         // device: permutation plan of the last pivot block
   PanelWs* panel_ws;     // device: exchange slots of the panel team
   LuState* lu_state;     // device: persistent-kernel state
@@ -419,6 +420,7 @@ struct PanelKArgs {
   double* P; int m, w; int64_t ld; int* ipiv; int b_inner;
   const unsigned* stop_flag; int stop_after_polls;
   PanelWs* ws; unsigned* ctrl; mla_lu_info* info;
+  int* sing_accum;   // nullable: OR-ed with the panel's singular flag (asynchronous callers)
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_panel(PanelKArgs a) {
@@ -438,6 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_panel(PanelKArgs a) {
     a.info->et_events = (r.cols_factored < a.w) ? 1 : 0;
     a.info->n_panels = 1;
     a.info->ws_joins = 0;
+    if (a.sing_accum && r.singular) atomicOr(a.sing_accum, 1);
   }
 }
 
@@ -465,13 +468,40 @@ extern "C" int mla_panel_ll(mla_handle h, double* P, int64_t m, int64_t w, int64
   if (grid > h->num_sms) grid = h->num_sms;
   if (grid > kMaxTeam) grid = kMaxTeam;
   CK(h, cudaMemsetAsync(h->ctrl, 0, CW_COUNT * sizeof(unsigned), s));
-  PanelKArgs a{P, (int)m, (int)w, ld, ipiv, b_inner, stop_flag, stop_after_polls, h->panel_ws, h->ctrl, h->info_dev};
+  PanelKArgs a{P, (int)m, (int)w, ld, ipiv, b_inner, stop_flag, stop_after_polls, h->panel_ws, h->ctrl, h->info_dev,
+               nullptr};
   void* args[] = {&a};
   CK(h, cudaLaunchCooperativeKernel((void*)k_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
   CK(h, cudaMemcpyAsync(h->info_host, h->info_dev, sizeof(mla_lu_info), cudaMemcpyDeviceToHost, s));
   int rc = check_abort(h, s);
   if (info) *info = *h->info_host;
   return rc;
+}
+
+extern "C" int mla_panel_ll_async(mla_handle h, double* P, int64_t m, int64_t w, int64_t ld, int32_t* ipiv,
+                                  int b_inner, int team_ctas, int32_t* singular_accum, void* stream) {
+  if (!h || m < w || w < 0 || b_inner < 1 || (m > 0 && ld < m)) return MLA_E_INVALID;
+  if (w == 0) return MLA_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(h, cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
+  int grid = team_ctas;
+  if (grid <= 0) {
+    int64_t want = (m + 255) / 256;
+    grid = (int)(want < 1 ? 1 : want);
+  }
+  if (grid > h->num_sms) grid = h->num_sms;
+  if (grid > kMaxTeam) grid = kMaxTeam;
+  CK(h, cudaMemsetAsync(h->ctrl, 0, CW_COUNT * sizeof(unsigned), s));
+  PanelKArgs a{P, (int)m, (int)w, ld, ipiv, b_inner, nullptr, 0, h->panel_ws, h->ctrl, h->info_dev, singular_accum};
+  void* args[] = {&a};
+  CK(h, cudaLaunchCooperativeKernel((void*)k_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
+  return MLA_OK;
+}
+
+extern "C" int mla_set_update_sms(mla_handle h, int ctas) {
+  if (!h || ctas < 0) return MLA_E_INVALID;
+  h->update_sms = ctas;
+  return MLA_OK;
 }
 
 // ---- getrf (persistent kernel) ----------------------------------------------------------------------
@@ -662,21 +692,44 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
   bulk_wait_all();
 }
 
+// prepare: interchange plan, empty queue, fresh flag tag.  launch: `ctas` CTAs (0 = update_sms / all) that
+// drain the prepared queue; a second launch of the same step (other stream) joins the same queue -- the
+// distributed driver's worker sharing: the SMs that factored the next panel join the update when done.
+extern "C" int mla_apply_panel_prepare(mla_handle h, const int32_t* ipiv, int64_t w, int64_t rows, void* stream) {
+  if (!h || rows < w || w < 0 || w > kMaxPiv) return MLA_E_INVALID;
+  if (w == 0) return MLA_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_laswp_plan<<<1, 32, 0, s>>>(ipiv, (int)w, rows, 0, h->plan, h->ctrl);
+  CK(h, cudaGetLastError());
+  CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
+  ++h->apply_tag;
+  return MLA_OK;
+}
+
+extern "C" int mla_apply_panel_launch(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
+                                      int64_t cols, int64_t ldt, int ctas, void* stream) {
+  if (!h || rows < w || w < 0 || cols < 0 || ctas < 0 || (rows > 0 && (ldp < rows || ldt < rows))) return MLA_E_INVALID;
+  if (w > kMaxPiv || cols > (int64_t)kMaxStrips * TRSM_CW) return MLA_E_INVALID;
+  if (w == 0 || cols == 0) return MLA_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(h, cudaFuncSetAttribute(k_apply_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
+  ApplyArgs a{P, ldp, (int)rows, (int)w, T, ldt, (int)cols, h->plan, h->ctrl, h->lu_state->rprep_done, h->apply_tag};
+  void* args[] = {&a};
+  int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
+  if (h->update_sms > 0 && h->update_sms < grid) grid = h->update_sms;
+  if (ctas > 0 && ctas < grid) grid = ctas;
+  CK(h, cudaLaunchCooperativeKernel((void*)k_apply_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
+  return MLA_OK;
+}
+
 extern "C" int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
                                int64_t cols, int64_t ldt, const int32_t* ipiv, void* stream) {
   if (!h || rows < w || w < 0 || cols < 0 || (rows > 0 && (ldp < rows || ldt < rows))) return MLA_E_INVALID;
   if (w > kMaxPiv || cols > (int64_t)kMaxStrips * TRSM_CW) return MLA_E_INVALID;
   if (w == 0 || cols == 0) return MLA_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  k_laswp_plan<<<1, 32, 0, s>>>(ipiv, (int)w, rows, 0, h->plan, h->ctrl);
-  CK(h, cudaGetLastError());
-  CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
-  CK(h, cudaFuncSetAttribute(k_apply_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
-  ApplyArgs a{P, ldp, (int)rows, (int)w, T, ldt, (int)cols, h->plan, h->ctrl, h->lu_state->rprep_done, ++h->apply_tag};
-  void* args[] = {&a};
-  int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
-  CK(h, cudaLaunchCooperativeKernel((void*)k_apply_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
-  return MLA_OK;
+  int rc = mla_apply_panel_prepare(h, ipiv, w, rows, stream);
+  if (rc != MLA_OK) return rc;
+  return mla_apply_panel_launch(h, P, rows, w, ldp, T, cols, ldt, 0, stream);
 }
 
 // ---- fill_random -----------------------------------------------------------------------------------

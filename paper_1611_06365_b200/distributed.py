@@ -102,12 +102,32 @@ class CudaOps:
         """laswp + trsm + gemm of one update step as ONE persistent launch (no host sync)."""
         self._k.apply_panel(panel, w, target, piv, pool=self.pool)
 
+    # ---- the owner's next panel beside its update (second handle = second set of control words) ----
+    def make_side_pool(self, device):
+        from .pool import SmPool, default_pool
+        self.pool = self.pool or default_pool(device.index)
+        self.side_pool = SmPool(device.index)
+        return self.side_pool
+
+    def panel_async(self, a, b_inner, team_sms, singular_accum):
+        """Stream-ordered panel on `team_sms` SMs of the side handle -> device pivots."""
+        return self._lu.lu_blk_ll_async(a, b_inner, self.side_pool, team_sms, singular_accum)
+
+    def set_update_sms(self, ctas):
+        self.pool.set_update_sms(ctas)
+
+    def apply_prepare(self, piv, w, rows, device):
+        self._k.apply_panel_prepare(piv, w, rows, device, pool=self.pool)
+
+    def apply_launch(self, panel, w, target, ctas):
+        self._k.apply_panel_launch(panel, w, target, ctas, pool=self.pool)
+
 
 class DistLU:
     """One rank's share of a block-cyclic LU.  `group` = process group (default WORLD)."""
 
     def __init__(self, n, b_outer, b_inner, cfg, device, variant="lu_la", pool=None, ops=None, group=None,
-                 rank=None, world=None):
+                 rank=None, world=None, panel_sms=32, comm_sms=8):
         self.n, self.b, self.b_inner, self.cfg = n, b_outer, b_inner, cfg
         self.device = torch.device(device)
         self.group = group
@@ -123,6 +143,19 @@ class DistLU:
         self.cuda = self.device.type == "cuda"
         self.comm_stream = torch.cuda.Stream(self.device) if self.cuda else None
         self.launches_per_factor = 0
+        # Look-ahead on the device (CUDA operator table only): the owner of block k+1 factors that panel
+        # on `panel_sms` SMs (side handle, side stream) WHILE it applies panel k to the rest of its
+        # columns on the other SMs; with P > 1 every rank's update also leaves `comm_sms` SMs to the
+        # NCCL kernels -- an update CTA takes a whole SM's shared memory, so on a full grid the broadcast
+        # could not start before the update ends.
+        self.overlap = self.cuda and hasattr(self.ops, "panel_async")
+        if self.overlap:
+            self.ops.make_side_pool(self.device)
+            self.panel_stream = torch.cuda.Stream(self.device)
+            self.sms = self.ops.pool.t
+            self.panel_sms = max(1, min(int(panel_sms), self.sms - 1))
+            self.comm_sms = int(comm_sms) if self.P > 1 else 0
+            self._sing_dev = torch.zeros(1, dtype=torch.int32, device=self.device)
         # two broadcast buffers (double buffering: panel k+1 is in flight while panel k is consumed)
         cap = n * b_outer + b_outer
         self.bufs = [torch.zeros(cap, dtype=torch.float64, device=self.device) for _ in range(2)]
@@ -217,6 +250,8 @@ class DistLU:
         self.launches_per_factor = 0
         self.singular = False
         self._piv_dev = torch.zeros(self.n, dtype=torch.int32, device=self.device)
+        if self.overlap:
+            self._sing_dev.zero_()
         nb = m.nblocks
         # panel 0
         cur = 0
@@ -232,7 +267,37 @@ class DistLU:
             self._piv_dev[j0:j0 + w] = piv + j0
             right_lo = m.local_start_after(self.rank, k)
             nxt = 1 - cur
-            if k + 1 < nb and m.owner(k + 1) == self.rank:
+            if k + 1 < nb and m.owner(k + 1) == self.rank and self.overlap:
+                # look-ahead with the panel BESIDE the update: block k+1 first (all SMs), then its
+                # panel on panel_sms SMs of the side stream while the rest of the columns are updated on
+                # the others; pack + broadcast follow the panel on their own streams
+                lo = m.local_offset(k + 1)
+                w1 = m.width(k + 1)
+                main = torch.cuda.current_stream(self.device)
+                self.ops.set_update_sms(0 if self.comm_sms == 0 else self.sms - self.comm_sms)
+                self._apply(k, panel, piv, lo, lo + w1)
+                self.panel_stream.wait_stream(main)
+                with torch.cuda.stream(self.panel_stream):
+                    j1 = (k + 1) * self.b
+                    piv1 = self.ops.panel_async(self.a[j1:, lo:lo + w1], self.b_inner, self.panel_sms, self._sing_dev)
+                    self.launches_per_factor += 1
+                    self._pack(self.bufs[nxt], k + 1, piv1)
+                self._start_bcast(nxt, k + 1, after=self.panel_stream)
+                self.ops.set_update_sms(0)
+                if self.nloc > lo + w1:
+                    # the rest of the update: G - panel_sms - comm_sms SMs now, and the panel's SMs JOIN the
+                    # same queue as soon as the panel is packed (worker sharing across two launches)
+                    tgt = self.a[j0:, lo + w1:self.nloc]
+                    self.ops.apply_prepare(piv, w, self.n - j0, self.device)
+                    ready = torch.cuda.Event()
+                    ready.record(main)
+                    self.ops.apply_launch(panel, w, tgt, self.sms - self.panel_sms - self.comm_sms)
+                    with torch.cuda.stream(self.panel_stream):
+                        self.panel_stream.wait_event(ready)
+                        self.ops.apply_launch(panel, w, tgt, self.panel_sms)
+                    self.launches_per_factor += 3
+                main.wait_stream(self.panel_stream)
+            elif k + 1 < nb and m.owner(k + 1) == self.rank:
                 # look-ahead: next panel's block first, factor it, start its broadcast early
                 lo = m.local_offset(k + 1)
                 w1 = m.width(k + 1)
@@ -245,7 +310,11 @@ class DistLU:
             else:
                 if k + 1 < nb:
                     self._start_bcast(nxt, k + 1)
+                if self.overlap and self.comm_sms:
+                    self.ops.set_update_sms(self.sms - self.comm_sms)
                 self._apply(k, panel, piv, right_lo, self.nloc)
+                if self.overlap and self.comm_sms:
+                    self.ops.set_update_sms(0)
             # interchanges for the owned columns left of the panel (lu.py:252, 329-332)
             left_hi = right_lo - (w if m.owner(k) == self.rank else 0)
             if left_hi > 0:
@@ -254,12 +323,14 @@ class DistLU:
             if k + 1 < nb:
                 self._finish_bcast()
             cur = nxt
+        if self.overlap:
+            self.singular |= bool(int(self._sing_dev.item()))
         self.ipiv = self._piv_dev.cpu().numpy().astype(np.int64)   # the only device->host copy
         return self.ipiv
 
-    def _start_bcast(self, which, k):
+    def _start_bcast(self, which, k, after=None):
         if self.cuda and self.P > 1:
-            self.comm_stream.wait_stream(torch.cuda.current_stream(self.device))
+            self.comm_stream.wait_stream(after if after is not None else torch.cuda.current_stream(self.device))
             with torch.cuda.stream(self.comm_stream):
                 self._bcast(self.bufs[which], k)
         else:

@@ -104,3 +104,27 @@ def apply_panel(panel: torch.Tensor, w: int, target: torch.Tensor, piv, pool=Non
     pool = pool or default_pool(target.device.index)
     _capi.check(_capi.lib().mla_apply_panel(pool.handle, panel.data_ptr(), rows, w, ldp, target.data_ptr(), cols,
                                             ldt, ip.data_ptr(), _stream(target)), pool.handle, "apply_panel")
+
+
+def apply_panel_prepare(piv, w: int, rows: int, device, pool=None, stream=None) -> None:
+    """First half of apply_panel (plan, queue, tag); see apply_panel_launch."""
+    pool = pool or default_pool(device.index)
+    ip = _device_pivots(piv, device)
+    if int(ip.shape[0]) < w:
+        raise ValueError("apply_panel: need w pivots")
+    st = torch.cuda.current_stream(device).cuda_stream if stream is None else stream
+    _capi.check(_capi.lib().mla_apply_panel_prepare(pool.handle, ip.data_ptr(), w, rows, st), pool.handle,
+                "apply_panel_prepare")
+
+
+def apply_panel_launch(panel: torch.Tensor, w: int, target: torch.Tensor, ctas: int = 0, pool=None) -> None:
+    """Second half of apply_panel on the current stream: `ctas` CTAs (0 = all) drain the prepared queue.
+    Launching it twice (two streams) makes the second launch join the first one's queue."""
+    rows, pw, ldp = check_colmajor(panel, "panel")
+    trows, cols, ldt = check_colmajor(target, "target")
+    if trows != rows or w > pw or w > rows:
+        raise ValueError("apply_panel: panel/target shapes disagree")
+    pool = pool or default_pool(target.device.index)
+    _capi.check(_capi.lib().mla_apply_panel_launch(pool.handle, panel.data_ptr(), rows, w, ldp, target.data_ptr(),
+                                                   cols, ldt, int(ctas), _stream(target)), pool.handle,
+                "apply_panel_launch")

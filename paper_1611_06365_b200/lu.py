@@ -90,6 +90,23 @@ def lu_unb(a: torch.Tensor, ipiv=None, pool: SmPool | None = None) -> LuResult:
     return lu_blk_ll(a, max(n, 1), pool=pool)
 
 
+def lu_blk_ll_async(a: torch.Tensor, b: int, pool: SmPool, team_sms: int = 0,
+                    singular_accum: torch.Tensor | None = None) -> torch.Tensor:
+    """Stream-ordered lu_blk_ll for drivers that never look at the result on the host: returns the
+    panel-local pivots as a device int32 tensor; `singular_accum` (device int32[1]) is OR-ed with the
+    singular flag.  No stop flag, no synchronisation."""
+    m, n, ld = _check_tall(a)
+    if b < 1:
+        raise ValueError("block size must be >= 1")
+    dev_piv = torch.empty(n, dtype=torch.int32, device=a.device)
+    if n == 0:
+        return dev_piv
+    acc = 0 if singular_accum is None else singular_accum.data_ptr()
+    _capi.check(_capi.lib().mla_panel_ll_async(pool.handle, a.data_ptr(), m, n, ld, dev_piv.data_ptr(), int(b),
+                                               int(team_sms), acc, _stream(a)), pool.handle, "lu_blk_ll_async")
+    return dev_piv
+
+
 def lu_blk_rl(a: torch.Tensor, b: int, ipiv=None, team=None, cfg=None, inner_b: int | None = None,
               pool: SmPool | None = None) -> LuResult:
     """Right-looking blocked LU (lu.py:106-137): panel, pivots left and right, trsm, gemm --

@@ -46,6 +46,11 @@ class SmPool:
                     "mla_set_panel_sms_max")
         self._t_pf_max = min(value, self.t - 1)
 
+    def set_update_sms(self, ctas: int) -> None:
+        """SMs that apply_panel launches on (0 = all): a multi-GPU driver keeps a few free for the
+        communication kernels and for the next panel running beside the update."""
+        _capi.check(_capi.lib().mla_set_update_sms(self.handle, int(ctas)), self._h, "mla_set_update_sms")
+
     @property
     def handle(self):
         if self._closed:
