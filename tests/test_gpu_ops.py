@@ -276,3 +276,32 @@ def test_apply_panel_equals_operator_chain(mla, rows, w, cols):
     oracle.gemm(ref[w:, :], panel[w:, :w], ref[:w, :], 1.0, -1.0)
     err, _ = lu_error(mla.to_numpy(a), ref)
     assert err <= 1e-10
+
+
+def test_apply_panel_second_launch_joins_the_queue(mla):
+    """Worker sharing across kernels (distributed driver): one update step prepared once, drained by a
+    launch on 100 SMs and a second launch on 40 SMs of another stream that joins the same queue; the
+    result is bitwise that of the single launch (one owner per tile either way)."""
+    from paper_1611_06365_b200.kernels import apply_panel, apply_panel_launch, apply_panel_prepare
+    rows, w, cols = 6000, 256, 5000
+    rng = np.random.default_rng(7)
+    panel = np.asfortranarray(rng.uniform(-1, 1, (rows, w)))
+    tgt = np.asfortranarray(rng.standard_normal((rows, cols)))
+    ipiv = np.array([rng.integers(t, rows) for t in range(w)], dtype=np.int64)
+    dp = mla.from_numpy(panel)
+    want = mla.from_numpy(tgt)
+    apply_panel(dp, w, want, ipiv)
+    got = mla.from_numpy(tgt)
+    piv_dev = torch.as_tensor(ipiv, dtype=torch.int32, device=got.device)
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    apply_panel_prepare(piv_dev, w, rows, got.device)
+    ready = torch.cuda.Event()
+    ready.record(main)
+    apply_panel_launch(dp, w, got, 100)
+    with torch.cuda.stream(side):
+        side.wait_event(ready)
+        apply_panel_launch(dp, w, got, 40)
+    main.wait_stream(side)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
