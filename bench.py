@@ -294,7 +294,7 @@ def run_ours(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"{name}: LU n={n} b={b_o}/{b_i} {cfg.dist} seed {cfg.seed}",
-                           "variant": args.variant, "layout": "1-D block-cyclic columns, NCCL panel+pivot broadcast",
+                           "variant": args.variant, "layout": "1-D block-cyclic columns, NCCL panel+pivot broadcast, next panel on 32 SMs beside the update",
                            "l2": "inputs larger than L2"},
                 "roofline": {"bound": "tensor", "achieved": round(val / 1e3, 3), "peak": FP64_TENSOR_PEAK_TFLOPS * world,
                              "unit": "TFLOP/s", "frac": round(val / 1e3 / (FP64_TENSOR_PEAK_TFLOPS * world), 4),
