@@ -123,8 +123,8 @@ int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int3
  * iteration, lu.py:270-273; WS only lends panel SMs to the update inside an iteration).
  * sm_pf_max > sm_pf additionally lets the panel team grow between iterations -- doubled, up to
  * sm_pf_max, after an iteration whose panel finished after the remainder update, halved (not below
- * sm_pf) after one whose panel took under a third of the iteration.  Pivots and factors do not depend
- * on the split.  Returns MLA_E_INVALID for negative values. */
+ * sm_pf) after one whose panel took under a third of the iteration.  Pivots do not depend on the
+ * split (factors: last-bit differences when the team size changes the panel's device block width).  Returns MLA_E_INVALID for negative values. */
 int mla_set_panel_sms_max(mla_handle h, int sm_pf_max);
 
 /* Same, reading the info back (synchronises the stream). */

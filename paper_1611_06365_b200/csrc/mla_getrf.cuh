@@ -401,8 +401,8 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
   // Panel-team size.  Fixed at sm_pf (the reference's t_pf, restored every iteration, lu.py:270-273),
   // or -- with sm_pf_max > sm_pf -- malleable between iterations: doubled after an iteration in which
   // the panel finished after the remainder update (the panel was the critical path), halved again
-  // after one in which it took less than a third of the iteration.  The factors do not depend on
-  // the team size (pivot search and every row's dot products are the same for any split).
+  // after one in which it took less than a third of the iteration.  The pivots do not depend on the
+  // team size; the factors only through the panel's device block width (slab fitting).
   const int sm_pf_lo = la ? imax(1, imin(a.sm_pf, G - 1)) : G;
   const int sm_pf_hi = la ? imax(sm_pf_lo, imin(a.sm_pf_max, G - 1)) : G;
   int sm_pf = sm_pf_lo;

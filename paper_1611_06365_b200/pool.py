@@ -4,7 +4,7 @@ The reference's pool is a set of CPU threads dispatched as one or two teams; her
 the SMs of one B200 and the dispatch happens inside the persistent kernel, so the pool only owns the
 library handle (workspace, flags, queues) and the default split.  `t` is the number of SMs, `t_pf`
 the default size of the panel team, `t_pf_max` how far the panel team may grow between iterations
-when the panel is the critical path (0 = fixed split, the reference's behaviour; the result does not
+when the panel is the critical path (0 = fixed split, the reference's behaviour; the pivots do not
 depend on it).  CompletionFlag is a device word (pool.py:28-49).
 """
 from __future__ import annotations
