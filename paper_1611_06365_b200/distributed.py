@@ -116,6 +116,10 @@ class CudaOps:
     def set_update_sms(self, ctas):
         self.pool.set_update_sms(ctas)
 
+    def laswp_side(self, a, ipiv):
+        """laswp through the side handle (its own plan buffer), for the side stream."""
+        self._k.laswp(a, ipiv, pool=self.side_pool, check=False)
+
     def apply_prepare(self, piv, w, rows, device):
         self._k.apply_panel_prepare(piv, w, rows, device, pool=self.pool)
 
@@ -267,6 +271,7 @@ class DistLU:
             self._piv_dev[j0:j0 + w] = piv + j0
             right_lo = m.local_start_after(self.rank, k)
             nxt = 1 - cur
+            left_done = False
             if k + 1 < nb and m.owner(k + 1) == self.rank and self.overlap:
                 # look-ahead with the panel BESIDE the update: block k+1 first (all SMs), then its
                 # panel on panel_sms SMs of the side stream while the rest of the columns are updated on
@@ -293,6 +298,13 @@ class DistLU:
                     ready.record(main)
                     self.ops.apply_launch(panel, w, tgt, self.sms - self.panel_sms - self.comm_sms)
                     with torch.cuda.stream(self.panel_stream):
+                        # the interchanges of the owned columns LEFT of panel k (lu.py:252) touch neither
+                        # the update's columns nor the new panel: the panel's SMs do them before joining
+                        left_hi = right_lo - (w if m.owner(k) == self.rank else 0)
+                        if left_hi > 0:
+                            self.ops.laswp_side(self.a[j0:, :left_hi], piv)
+                            self.launches_per_factor += 1
+                            left_done = True
                         self.panel_stream.wait_event(ready)
                         self.ops.apply_launch(panel, w, tgt, self.panel_sms)
                     self.launches_per_factor += 3
@@ -317,7 +329,7 @@ class DistLU:
                     self.ops.set_update_sms(0)
             # interchanges for the owned columns left of the panel (lu.py:252, 329-332)
             left_hi = right_lo - (w if m.owner(k) == self.rank else 0)
-            if left_hi > 0:
+            if left_hi > 0 and not left_done:
                 self.ops.laswp(self.a[j0:, :left_hi], piv)
                 self.launches_per_factor += 1
             if k + 1 < nb:
