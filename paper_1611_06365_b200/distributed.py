@@ -116,6 +116,11 @@ class CudaOps:
     def set_update_sms(self, ctas):
         self.pool.set_update_sms(ctas)
 
+    def apply_panel_side(self, panel, w, target, piv, ctas):
+        """apply_panel through the side handle on `ctas` SMs (for the side stream)."""
+        self.side_pool.set_update_sms(ctas)
+        self._k.apply_panel(panel, w, target, piv, pool=self.side_pool)
+
     def laswp_side(self, a, ipiv):
         """laswp through the side handle (its own plan buffer), for the side stream."""
         self._k.laswp(a, ipiv, pool=self.side_pool, check=False)
@@ -273,41 +278,42 @@ class DistLU:
             nxt = 1 - cur
             left_done = False
             if k + 1 < nb and m.owner(k + 1) == self.rank and self.overlap:
-                # look-ahead with the panel BESIDE the update: block k+1 first (all SMs), then its
-                # panel on panel_sms SMs of the side stream while the rest of the columns are updated on
-                # the others; pack + broadcast follow the panel on their own streams
+                # Look-ahead on the device.  Side stream, panel_sms SMs (side handle): panel k applied to
+                # block k+1, panel k+1 factored, packed, its broadcast started, the LEFT interchanges of
+                # panel k -- then those SMs JOIN the main update's queue with a second launch.  Main
+                # stream, the other SMs: panel k applied to the rest of the owned columns, from the start.
                 lo = m.local_offset(k + 1)
                 w1 = m.width(k + 1)
+                j1 = (k + 1) * self.b
                 main = torch.cuda.current_stream(self.device)
-                self.ops.set_update_sms(0 if self.comm_sms == 0 else self.sms - self.comm_sms)
-                self._apply(k, panel, piv, lo, lo + w1)
                 self.panel_stream.wait_stream(main)
-                with torch.cuda.stream(self.panel_stream):
-                    j1 = (k + 1) * self.b
-                    piv1 = self.ops.panel_async(self.a[j1:, lo:lo + w1], self.b_inner, self.panel_sms, self._sing_dev)
-                    self.launches_per_factor += 1
-                    self._pack(self.bufs[nxt], k + 1, piv1)
-                self._start_bcast(nxt, k + 1, after=self.panel_stream)
-                self.ops.set_update_sms(0)
-                if self.nloc > lo + w1:
-                    # the rest of the update: G - panel_sms - comm_sms SMs now, and the panel's SMs JOIN the
-                    # same queue as soon as the panel is packed (worker sharing across two launches)
+                have_rest = self.nloc > lo + w1
+                if have_rest:
                     tgt = self.a[j0:, lo + w1:self.nloc]
+                    self.ops.set_update_sms(0)
                     self.ops.apply_prepare(piv, w, self.n - j0, self.device)
                     ready = torch.cuda.Event()
                     ready.record(main)
                     self.ops.apply_launch(panel, w, tgt, self.sms - self.panel_sms - self.comm_sms)
-                    with torch.cuda.stream(self.panel_stream):
-                        # the interchanges of the owned columns LEFT of panel k (lu.py:252) touch neither
-                        # the update's columns nor the new panel: the panel's SMs do them before joining
-                        left_hi = right_lo - (w if m.owner(k) == self.rank else 0)
-                        if left_hi > 0:
-                            self.ops.laswp_side(self.a[j0:, :left_hi], piv)
-                            self.launches_per_factor += 1
-                            left_done = True
+                    self.launches_per_factor += 2
+                with torch.cuda.stream(self.panel_stream):
+                    self.ops.apply_panel_side(panel, w, self.a[j0:, lo:lo + w1], piv, self.panel_sms)
+                    piv1 = self.ops.panel_async(self.a[j1:, lo:lo + w1], self.b_inner, self.panel_sms, self._sing_dev)
+                    self._pack(self.bufs[nxt], k + 1, piv1)
+                    self.launches_per_factor += 3
+                self._start_bcast(nxt, k + 1, after=self.panel_stream)
+                with torch.cuda.stream(self.panel_stream):
+                    # the interchanges of the owned columns LEFT of panel k (lu.py:252) touch neither the
+                    # update's columns nor the new panel
+                    left_hi = right_lo - (w if m.owner(k) == self.rank else 0)
+                    if left_hi > 0:
+                        self.ops.laswp_side(self.a[j0:, :left_hi], piv)
+                        self.launches_per_factor += 1
+                        left_done = True
+                    if have_rest:
                         self.panel_stream.wait_event(ready)
                         self.ops.apply_launch(panel, w, tgt, self.panel_sms)
-                    self.launches_per_factor += 3
+                        self.launches_per_factor += 1
                 main.wait_stream(self.panel_stream)
             elif k + 1 < nb and m.owner(k + 1) == self.rank:
                 # look-ahead: next panel's block first, factor it, start its broadcast early
