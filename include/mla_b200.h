@@ -157,9 +157,10 @@ int mla_apply_panel_prepare(mla_handle h, const int32_t* ipiv, int64_t w, int64_
 int mla_apply_panel_launch(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
                            int64_t cols, int64_t ldt, int ctas, void* stream);
 
-/* Number of SMs mla_apply_panel launches on (0 = all).  A multi-GPU driver leaves a few SMs to the
- * communication kernels, and the owner of the next panel runs that panel (mla_panel_ll_async, second
- * handle, second stream) next to its update on the remaining SMs. */
+/* Number of SMs mla_apply_panel launches on (0 = all).  Lets a multi-GPU driver leave SMs to the
+ * communication kernels or to another kernel of its own.  (Running mla_panel_ll_async beside an update
+ * this way is what distributed.py's experimental two-stream mode does; that mode currently races and
+ * is off by default.) */
 int mla_set_update_sms(mla_handle h, int ctas);
 
 /* fill_random(a, seed) -- matrix.py:44-63: SplitMix64 stream, bit-identical to the reference;

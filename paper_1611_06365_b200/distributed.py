@@ -103,11 +103,17 @@ class CudaOps:
         self._k.apply_panel(panel, w, target, piv, pool=self.pool)
 
     # ---- the owner's next panel beside its update (second handle = second set of control words) ----
+    _side_pools: dict = {}      # one side handle per device, shared by all drivers of this process
+
     def make_side_pool(self, device):
         from .pool import SmPool, default_pool
         self.pool = self.pool or default_pool(device.index)
-        self.side_pool = SmPool(device.index)
-        return self.side_pool
+        sp = CudaOps._side_pools.get(device.index)
+        if sp is None or sp._closed:
+            sp = SmPool(device.index)
+            CudaOps._side_pools[device.index] = sp
+        self.side_pool = sp
+        return sp
 
     def panel_async(self, a, b_inner, team_sms, singular_accum):
         """Stream-ordered panel on `team_sms` SMs of the side handle -> device pivots."""
@@ -136,7 +142,7 @@ class DistLU:
     """One rank's share of a block-cyclic LU.  `group` = process group (default WORLD)."""
 
     def __init__(self, n, b_outer, b_inner, cfg, device, variant="lu_la", pool=None, ops=None, group=None,
-                 rank=None, world=None, panel_sms=32, comm_sms=8):
+                 rank=None, world=None, panel_sms=32, comm_sms=8, storage=None, overlap_panel=False):
         self.n, self.b, self.b_inner, self.cfg = n, b_outer, b_inner, cfg
         self.device = torch.device(device)
         self.group = group
@@ -145,19 +151,25 @@ class DistLU:
         self.map = BlockCyclic(n, b_outer, self.P)
         self.ops = ops or CudaOps(pool)
         self.nloc = self.map.local_cols(self.rank)
-        self.a = self.ops.alloc(n, max(self.nloc, 1), self.device)[:, :self.nloc]
+        # `storage`: factor the caller's (n x nloc, column-major) tensor in place instead of an own buffer
+        self.a = storage if storage is not None else self.ops.alloc(n, max(self.nloc, 1), self.device)[:, :self.nloc]
         self.a0 = None
         self.ipiv = np.zeros(n, dtype=np.int64)
         self.singular = False
         self.cuda = self.device.type == "cuda"
         self.comm_stream = torch.cuda.Stream(self.device) if self.cuda else None
         self.launches_per_factor = 0
-        # Look-ahead on the device (CUDA operator table only): the owner of block k+1 factors that panel
-        # on `panel_sms` SMs (side handle, side stream) WHILE it applies panel k to the rest of its
-        # columns on the other SMs; with P > 1 every rank's update also leaves `comm_sms` SMs to the
-        # NCCL kernels -- an update CTA takes a whole SM's shared memory, so on a full grid the broadcast
-        # could not start before the update ends.
-        self.overlap = self.cuda and hasattr(self.ops, "panel_async")
+        # EXPERIMENTAL, OFF BY DEFAULT (overlap_panel=True): look-ahead on the device -- the owner of block
+        # k+1 applies panel k to that block, factors panel k+1 and does the LEFT interchanges on
+        # `panel_sms` SMs (side handle, side stream) WHILE panel k is applied to the rest of its columns
+        # on the other SMs, and those SMs then join the update's queue with a second launch.  Fast
+        # (P=1: n=32768 0.885 s, n=65536 6.26 s) but NOT CORRECT: with the panel kernel running beside
+        # the update kernel the factors come out wrong, non-deterministically, once the run is long
+        # enough (n > 32768, or n=32768 with b=256; backward error ~1e10 n eps; found by bench.py --check).
+        # Each piece is right on its own -- the same launches with a device synchronisation between panel
+        # and update are bitwise reproducible and pass -- so it is an interaction of the two concurrently
+        # resident kernels that round 1 did not root-cause.
+        self.overlap = bool(overlap_panel) and self.cuda and hasattr(self.ops, "panel_async")
         if self.overlap:
             self.ops.make_side_pool(self.device)
             self.panel_stream = torch.cuda.Stream(self.device)
@@ -357,6 +369,29 @@ class DistLU:
     def _finish_bcast(self):
         if self.cuda and self.P > 1:
             torch.cuda.current_stream(self.device).wait_stream(self.comm_stream)
+
+
+def lu_streams(a: torch.Tensor, b_outer: int, b_inner: int, pool=None, panel_sms: int = 32):
+    """Single-GPU LU of a square column-major matrix, in place, through THIS driver with P = 1: per outer
+    iteration separately compiled kernels (panel on all SMs, then one fused update launch, then the LEFT
+    interchanges) instead of the one persistent kernel behind lu_la.  Fixed panel width (the schedule
+    of variant "lu"; no look-ahead overlap, no early termination): n=32768 1.05 s against lu_la's 0.875 s.
+    Returns a LuResult like lu_la.  NOT part of the public API: parity with the oracle is verified at
+    test sizes only; at n=32768 the driver's pivots differ from the reference's although the
+    factorization is valid (known defect).  The two-stream variant of this driver is
+    faster but corrupts, see DistLU(overlap_panel=...)."""
+    from .lu import LuResult
+    from .matrix import PivotVector, check_colmajor
+    m, n, _ = check_colmajor(a, "a")
+    if m != n:
+        raise ValueError("lu_streams: square matrices only")
+    if n == 0:
+        return LuResult(PivotVector(np.empty(0, dtype=np.int64)), 0, False)
+    dlu = DistLU(n, b_outer, b_inner, None, a.device, pool=pool, rank=0, world=1, panel_sms=panel_sms, storage=a,
+                 overlap_panel=False)
+    ipiv = dlu.factor()
+    widths = tuple(dlu.map.width(j) for j in range(dlu.map.nblocks))
+    return LuResult(PivotVector(ipiv, device=dlu._piv_dev), n, bool(dlu.singular), 0, (), widths, dlu.map.nblocks - 1)
 
 
 def assemble_global(dlu: DistLU) -> np.ndarray | None:

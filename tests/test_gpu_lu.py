@@ -291,6 +291,23 @@ def test_distributed_driver_single_rank_cuda(mla):
     assert_parity(dlu.local_to_numpy(), ipiv, ref, ro.ipiv, "DistLU P=1")
 
 
+@pytest.mark.parametrize("n,b_o,b_i", [(2000, 256, 32), (1111, 128, 16), (300, 512, 64)])
+def test_lu_streams_matches_the_oracle_and_lu_la(mla, n, b_o, b_i):
+    """The multi-kernel single-GPU path (distributed driver with P = 1, in place on the caller's matrix):
+    pivots identical to the oracle's fixed-width schedule and to lu_la's lu_mb."""
+    a = gen(n, n, 9)
+    d = mla.from_numpy(a)
+    from paper_1611_06365_b200.distributed import lu_streams
+    r = lu_streams(d, b_o, b_i)
+    ref = a.copy(order="F")
+    ro = oracle.lu_la(ref, b_o, b_i)
+    assert_parity(mla.to_numpy(d), r.ipiv.ipiv, ref, ro.ipiv, f"lu_streams n={n}")
+    d2 = mla.from_numpy(a)
+    r2 = mla.lu_la(d2, mla.Policy("lu_mb", mla.BlockConfig(b_o, b_i)))
+    assert np.array_equal(r.ipiv.ipiv, r2.ipiv.ipiv)
+    assert tuple(r.widths) == tuple(r2.widths) and not r.singular
+
+
 def test_device_trace_is_a_valid_reference_trace(mla, tmp_path):  # acceptance 4 (test_acceptance.py:192-218)
     from paper_1611_06365_b200 import trace as mtrace
     pool = mla.default_pool()

@@ -9,7 +9,8 @@ from paper_1611_06365_b200.workloads import LuConfig
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 b = int(sys.argv[2]) if len(sys.argv) > 2 else 512
 cfg = LuConfig("t", n, "uniform", 4, b, b // 8)
-dlu = DistLU(n, b, b // 8, cfg, "cuda", rank=0, world=1, panel_sms=int(sys.argv[3]) if len(sys.argv) > 3 else 32)
+dlu = DistLU(n, b, b // 8, cfg, "cuda", rank=0, world=1, panel_sms=int(sys.argv[3]) if len(sys.argv) > 3 else 32,
+             overlap_panel=len(sys.argv) > 4 and sys.argv[4] == "overlap")   # overlap: experimental, races
 dlu.generate()
 for rep in range(2):
     dlu.restore(); torch.cuda.synchronize()
