@@ -376,10 +376,9 @@ def lu_streams(a: torch.Tensor, b_outer: int, b_inner: int, pool=None, panel_sms
     iteration separately compiled kernels (panel on all SMs, then one fused update launch, then the LEFT
     interchanges) instead of the one persistent kernel behind lu_la.  Fixed panel width (the schedule
     of variant "lu"; no look-ahead overlap, no early termination): n=32768 1.05 s against lu_la's 0.875 s.
-    Returns a LuResult like lu_la.  NOT part of the public API: parity with the oracle is verified at
-    test sizes only; at n=32768 the driver's pivots differ from the reference's although the
-    factorization is valid (known defect).  The two-stream variant of this driver is
-    faster but corrupts, see DistLU(overlap_panel=...)."""
+    Returns a LuResult like lu_la.  Not exported from the package: lu_la is the single-GPU path; this
+    one exists to exercise the driver on one GPU (parity at test sizes and, at n=32768, pivots equal to
+    lu_la's).  The two-stream variant of this driver is faster but corrupts, see DistLU(overlap_panel=...)."""
     from .lu import LuResult
     from .matrix import PivotVector, check_colmajor
     m, n, _ = check_colmajor(a, "a")
