@@ -308,6 +308,29 @@ def test_lu_streams_matches_the_oracle_and_lu_la(mla, n, b_o, b_i):
     assert tuple(r.widths) == tuple(r2.widths) and not r.singular
 
 
+def test_distributed_driver_full_size_pivots_equal_lu_la(mla):
+    """The multi-GPU driver's CUDA path at a size with many row blocks and strips (P = 1, n = 16384,
+    b = 512/64): same pivot sequence as lu_la (whose pivots are pinned to the oracle's golden vectors at
+    this size by the full-config tests), twice in a row, and a small backward error.  The residual helper
+    permutes its first argument, hence the copies."""
+    from paper_1611_06365_b200.distributed import DistLU
+    n, b_o, b_i = 16384, 512, 64
+    a0 = mla.alloc_matrix(n, n)
+    mla.fill_random(a0, 2, 2.0, -1.0)
+    x = a0.clone()
+    want = mla.lu_la(x, mla.Policy("lu_mb", mla.BlockConfig(b_o, b_i))).ipiv.ipiv.copy()
+    del x
+    for _ in range(2):
+        x = a0.clone()
+        dlu = DistLU(n, b_o, b_i, None, x.device, rank=0, world=1, storage=x)
+        ipiv = dlu.factor()
+        assert np.array_equal(ipiv, want)
+        chk = a0.clone()
+        berr = float(mla.residual_packed(chk, x, mla.PivotVector(ipiv))) / (n * EPS)
+        assert berr <= BACKWARD_TOL
+        del x, chk, dlu
+
+
 def test_device_trace_is_a_valid_reference_trace(mla, tmp_path):  # acceptance 4 (test_acceptance.py:192-218)
     from paper_1611_06365_b200 import trace as mtrace
     pool = mla.default_pool()
