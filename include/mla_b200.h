@@ -157,6 +157,10 @@ int mla_apply_panel_prepare(mla_handle h, const int32_t* ipiv, int64_t w, int64_
 int mla_apply_panel_launch(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
                            int64_t cols, int64_t ldt, int ctas, void* stream);
 
+/* The device-side abort word of the handle (0 = no watchdog / protocol abort since the last launch that
+ * reset it); the asynchronous entry points never read it back themselves.  Synchronises the device. */
+int mla_abort_word(mla_handle h);
+
 /* Number of SMs mla_apply_panel launches on (0 = all).  Lets a multi-GPU driver leave SMs to the
  * communication kernels or to another kernel of its own.  (Running mla_panel_ll_async beside an update
  * this way is what distributed.py's experimental two-stream mode does; that mode currently races and

@@ -66,6 +66,8 @@ def lib() -> ctypes.CDLL:
     L.mla_apply_panel_prepare.restype = ctypes.c_int
     L.mla_apply_panel_launch.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, ctypes.c_int, _vp]
     L.mla_apply_panel_launch.restype = ctypes.c_int
+    L.mla_abort_word.argtypes = [_vp]
+    L.mla_abort_word.restype = ctypes.c_int
     L.mla_set_update_sms.argtypes = [_vp, ctypes.c_int]
     L.mla_set_update_sms.restype = ctypes.c_int
     L.mla_set_panel_sms_max.argtypes = [_vp, ctypes.c_int]
@@ -86,7 +88,7 @@ EXPORTS = ("mla_version", "mla_create", "mla_destroy", "mla_num_sms", "mla_last_
            "mla_gemm", "mla_trsm_llu", "mla_laswp", "mla_panel_ll", "mla_getrf_la",
            "mla_getrf_la_sync", "mla_getrf_la_host", "mla_fill_random", "mla_panel_profile", "mla_getrf_trace", "mla_laswp_async", "mla_getrf_debug",
            "mla_gemm_half_experiment", "mla_apply_panel", "mla_set_panel_sms_max", "mla_panel_ll_async",
-           "mla_set_update_sms", "mla_apply_panel_prepare", "mla_apply_panel_launch")
+           "mla_set_update_sms", "mla_apply_panel_prepare", "mla_apply_panel_launch", "mla_abort_word")
 
 
 class MlaError(RuntimeError):

@@ -498,6 +498,14 @@ extern "C" int mla_panel_ll_async(mla_handle h, double* P, int64_t m, int64_t w,
   return MLA_OK;
 }
 
+extern "C" int mla_abort_word(mla_handle h) {
+  if (!h) return MLA_E_INVALID;
+  unsigned v = 0;
+  if (cudaDeviceSynchronize() != cudaSuccess) return MLA_E_CUDA;
+  if (cudaMemcpy(&v, h->ctrl + CW_ABORT, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return MLA_E_CUDA;
+  return (int)(v & 0x7fffffffu);
+}
+
 extern "C" int mla_set_update_sms(mla_handle h, int ctas) {
   if (!h || ctas < 0) return MLA_E_INVALID;
   h->update_sms = ctas;
