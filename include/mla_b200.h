@@ -191,13 +191,6 @@ int mla_getrf_trace(mla_handle h, uint64_t* out, int max_rows);
  * bookkeeping, [6] whole kernel. */
 int mla_getrf_debug(mla_handle h, uint64_t* out8);
 
-/* EXPERIMENT kept for the record (tools/dev_gemm_half.py): C -= A*B with the same tile
- * engine run as 128-thread CTAs on 128x64 tiles, two CTAs per SM, so that one CTA's epilogue overlaps
- * the other's DMMA stream (+5 % over mla_gemm at k=256); mode 1: the same as two independent 128-thread
- * groups inside one 256-thread CTA (named barriers, split ring).  Not used by the LU path. */
-int mla_gemm_half_experiment(mla_handle h, double* C, int64_t m, int64_t n, int64_t ldc, const double* A,
-                             int64_t lda, const double* B, int64_t ldb, int64_t k, int mode, void* stream);
-
 /* residual_lu (matrix.py:116-131) has no entry point of its own: the Python layer composes it from
  * mla_laswp (P*A) and mla_gemm (blocked L*U), see paper_1611_06365_b200/matrix.py. */
 

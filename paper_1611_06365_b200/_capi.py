@@ -56,8 +56,6 @@ def lib() -> ctypes.CDLL:
                                   ctypes.c_double, ctypes.c_double, _vp, _vp]
     L.mla_getrf_trace.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     L.mla_getrf_trace.restype = ctypes.c_int
-    L.mla_gemm_half_experiment.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, ctypes.c_int, _vp]
-    L.mla_gemm_half_experiment.restype = ctypes.c_int
     L.mla_apply_panel.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp]
     L.mla_apply_panel.restype = ctypes.c_int
     L.mla_panel_ll_async.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, ctypes.c_int, ctypes.c_int, _vp, _vp]
@@ -87,7 +85,7 @@ def lib() -> ctypes.CDLL:
 EXPORTS = ("mla_version", "mla_create", "mla_destroy", "mla_num_sms", "mla_last_cuda_error",
            "mla_gemm", "mla_trsm_llu", "mla_laswp", "mla_panel_ll", "mla_getrf_la",
            "mla_getrf_la_sync", "mla_getrf_la_host", "mla_fill_random", "mla_panel_profile", "mla_getrf_trace", "mla_laswp_async", "mla_getrf_debug",
-           "mla_gemm_half_experiment", "mla_apply_panel", "mla_set_panel_sms_max", "mla_panel_ll_async",
+           "mla_apply_panel", "mla_set_panel_sms_max", "mla_panel_ll_async",
            "mla_set_update_sms", "mla_apply_panel_prepare", "mla_apply_panel_launch", "mla_abort_word")
 
 

@@ -196,94 +196,6 @@ k_gemm(GemmProblem p, unsigned* ctrl, const unsigned* join_flag, int donors) {
   bulk_wait_all();   // this CTA's reductions into C are performed before the kernel retires
 }
 
-// EXPERIMENT (tools/dev_gemm_half.py): the same tile engine as 128-thread CTAs on 128x64 tiles, two CTAs
-// per SM, so that one CTA's epilogue / barrier bubbles overlap the other's DMMA stream.
-__global__ void __launch_bounds__(128, 2)
-k_gemm_half(GemmProblem p, unsigned* ctrl) {
-  extern __shared__ __align__(16) double smem[];
-  __shared__ int s_tile;
-  using Cfg = GemmHalfCfg;
-  const int ntiles = gemm_num_tiles<Cfg>(p);
-  auto pop = [&]() {
-    if (threadIdx.x == 0) s_tile = (int)atomicAdd(ctrl + CW_QUEUE_NEXT, 1u);
-    __syncthreads();
-    int t = s_tile;
-    __syncthreads();
-    return t;
-  };
-  int t = pop();
-  if (t >= ntiles) return;
-  TileDesc cur = gemm_tile_desc<Cfg>(p, t);
-  int base = 0;
-  tile_prologue<Cfg>(cur, base, smem);
-  while (true) {
-    int tn = pop();
-    TileDesc nxt{};
-    nxt.valid = false;
-    if (tn < ntiles && tile_kt<Cfg>(cur) >= Cfg::STAGES - 1) nxt = gemm_tile_desc<Cfg>(p, tn);
-    base = tile_run<Cfg>(cur, nxt, base, smem);
-    if (nxt.valid) { cur = nxt; continue; }
-    if (tn >= ntiles) break;
-    cur = gemm_tile_desc<Cfg>(p, tn);
-    base = 0;
-    tile_prologue<Cfg>(cur, base, smem);
-  }
-  bulk_wait_all();
-}
-
-// Same idea inside ONE 256-thread CTA: two independent 128-thread groups, each with its own ring and its
-// own named barrier, each pulling 128x64 half-tiles from the queue.
-__global__ void __launch_bounds__(kThreads, 1)
-k_gemm_dual(GemmProblem p, unsigned* ctrl) {
-  extern __shared__ __align__(16) double smem[];
-  __shared__ int s_tile[2];
-  using Cfg = GemmHalfCfg;
-  const int g = grp_id<Cfg::THREADS>(), gtid = grp_tid<Cfg::THREADS>();
-  double* gsmem = smem + g * (Cfg::SMEM_BYTES / 8);
-  const int ntiles = gemm_num_tiles<Cfg>(p);
-  auto pop = [&]() {
-    if (gtid == 0) s_tile[g] = (int)atomicAdd(ctrl + CW_QUEUE_NEXT, 1u);
-    grp_sync<Cfg::THREADS>();
-    int t = s_tile[g];
-    grp_sync<Cfg::THREADS>();
-    return t;
-  };
-  int t = pop();
-  if (t >= ntiles) return;
-  TileDesc cur = gemm_tile_desc<Cfg>(p, t);
-  int base = 0;
-  tile_prologue<Cfg>(cur, base, gsmem);
-  while (true) {
-    int tn = pop();
-    TileDesc nxt{};
-    nxt.valid = false;
-    if (tn < ntiles && tile_kt<Cfg>(cur) >= Cfg::STAGES - 1) nxt = gemm_tile_desc<Cfg>(p, tn);
-    base = tile_run<Cfg>(cur, nxt, base, gsmem);
-    if (nxt.valid) { cur = nxt; continue; }
-    if (tn >= ntiles) break;
-    cur = gemm_tile_desc<Cfg>(p, tn);
-    base = 0;
-    tile_prologue<Cfg>(cur, base, gsmem);
-  }
-  bulk_wait_all();
-}
-
-extern "C" int mla_gemm_half_experiment(mla_handle h, double* C, int64_t m, int64_t n, int64_t ldc, const double* A,
-                                        int64_t lda, const double* B, int64_t ldb, int64_t k, int mode, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  GemmProblem p{C, ldc, A, lda, B, ldb, (int)m, (int)n, (int)k, 1.0, -1.0};
-  CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
-  if (mode == 0) {
-    CK(h, cudaFuncSetAttribute(k_gemm_half, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmHalfCfg::SMEM_BYTES));
-    k_gemm_half<<<2 * h->num_sms, 128, GemmHalfCfg::SMEM_BYTES, s>>>(p, h->ctrl);
-  } else {
-    CK(h, cudaFuncSetAttribute(k_gemm_dual, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * GemmHalfCfg::SMEM_BYTES));
-    k_gemm_dual<<<h->num_sms, kThreads, 2 * GemmHalfCfg::SMEM_BYTES, s>>>(p, h->ctrl);
-  }
-  CK(h, cudaGetLastError());
-  return MLA_OK;
-}
-
 __global__ void k_scale(double* C, int64_t m, int64_t n, int64_t ldc, double alpha) {
   for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
@@ -346,10 +258,33 @@ extern "C" int mla_trsm_llu(mla_handle h, const double* L, int64_t w, int64_t ld
 }
 
 // ---- laswp -----------------------------------------------------------------------------------------
-__global__ void k_laswp_plan(const int* ipiv, int npiv, int64_t rows, int reverse, PivPlan* plan, unsigned* ctrl) {
+// Range check of a whole pivot vector (used when it is applied in chunks: NOTHING may be touched if
+// ANY index is bad, kernels.py:326-327, so the verdict must exist before the first chunk's plan).
+__global__ void k_laswp_validate(const int* ipiv, int64_t npiv, int64_t rows, unsigned* ctrl) {
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  bool bad = npiv > rows;
+  for (int64_t t = threadIdx.x; t < npiv; t += blockDim.x) {
+    int p = ipiv[t];
+    if (p < 0 || (int64_t)p >= rows) bad = true;
+  }
+  if (bad) s_bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) ctrl[CW_ERR_INDEX] = s_bad ? 1u : 0u;
+}
+
+// Plan of chunk [t0, t0+npiv) of a pivot vector.  prevalidated: a k_laswp_validate verdict is already in
+// ctrl[CW_ERR_INDEX] and, if bad, every chunk's plan must come out empty.
+__global__ void k_laswp_plan(const int* ipiv, int npiv, int64_t rows, int reverse, int t0, int prevalidated,
+                             PivPlan* plan, unsigned* ctrl) {
   __shared__ int top[kMaxPiv], pv[kMaxPiv], keys[2 * kMaxPiv], vals[2 * kMaxPiv];
-  bool ok = build_pivot_plan(ipiv, npiv, rows, reverse != 0, plan->ref(), top, keys, vals, 2 * kMaxPiv, pv);
-  if (threadIdx.x == 0) ctrl[CW_ERR_INDEX] = ok ? 0u : 1u;
+  if (prevalidated && ctrl[CW_ERR_INDEX] != 0u) {
+    if (threadIdx.x == 0) plan->count = 0;
+    return;
+  }
+  bool ok = build_pivot_plan(ipiv, npiv, rows, reverse != 0, plan->ref(), top, keys, vals, 2 * kMaxPiv, pv, t0);
+  if (threadIdx.x == 0 && !prevalidated) ctrl[CW_ERR_INDEX] = ok ? 0u : 1u;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -380,25 +315,24 @@ static int laswp_impl(mla_handle h, double* A, int64_t rows, int64_t cols, int64
                       int64_t npiv, int reverse, void* stream, bool readback) {
   if (!h || rows < 0 || cols < 0 || npiv < 0 || (rows > 0 && ld < rows)) return MLA_E_INVALID;
   if (npiv == 0) return MLA_OK;
+  if (!ipiv || rows >= (1ll << 31)) return MLA_E_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   const int smem_bytes = kLaswpBufDoubles * 8;
   CK(h, cudaFuncSetAttribute(k_laswp_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-  // pivot blocks wider than one plan are applied as consecutive chunks (ascending for forward,
-  // descending for reverse); chunk c works on the view that starts at its first row.
-  int64_t nchunks = (npiv + kMaxPiv - 1) / kMaxPiv;
-  int rc = MLA_OK;
+  // Pivot vectors longer than one plan (kMaxPiv) are applied as consecutive chunks of the SAME view
+  // (ascending for forward, descending for reverse); the whole vector is range-checked on the device
+  // first, and a bad index anywhere empties every chunk's plan, so nothing is touched.
+  const int64_t nchunks = (npiv + kMaxPiv - 1) / kMaxPiv;
+  const int preval = nchunks > 1 ? 1 : 0;
+  if (preval) {
+    k_laswp_validate<<<1, 256, 0, s>>>(ipiv, npiv, rows, h->ctrl);
+    CK(h, cudaGetLastError());
+  }
   for (int64_t ci = 0; ci < nchunks; ++ci) {
-    int64_t c = reverse ? (nchunks - 1 - ci) : ci;
-    int64_t t0 = c * kMaxPiv;
-    int np = (int)(npiv - t0 < kMaxPiv ? npiv - t0 : kMaxPiv);
-    if (c == 0) {
-      k_laswp_plan<<<1, 32, 0, s>>>(ipiv, np, rows, reverse, h->plan, h->ctrl);
-    } else {
-      // indices of later chunks are relative to row 0 of the view: rebase by -t0 on the fly is
-      // not possible without a copy, so chunked plans are only offered when the caller's pivots
-      // are already chunk-local.  (The LU path never needs more than kMaxPiv pivots per block.)
-      return MLA_E_INVALID;
-    }
+    const int64_t c = reverse ? (nchunks - 1 - ci) : ci;
+    const int64_t t0 = c * kMaxPiv;
+    const int np = (int)(npiv - t0 < kMaxPiv ? npiv - t0 : kMaxPiv);
+    k_laswp_plan<<<1, 32, 0, s>>>(ipiv + t0, np, rows, reverse, (int)t0, preval, h->plan, h->ctrl);
     CK(h, cudaGetLastError());
     if (cols > 0 && rows > 0) {
       int64_t want = (cols + 15) / 16;
@@ -408,11 +342,10 @@ static int laswp_impl(mla_handle h, double* A, int64_t rows, int64_t cols, int64
       CK(h, cudaGetLastError());
     }
   }
-  if (!readback) return rc;
+  if (!readback) return MLA_OK;
   CK(h, cudaMemcpyAsync(h->ctrl_host + CW_ERR_INDEX, h->ctrl + CW_ERR_INDEX, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   CK(h, cudaStreamSynchronize(s));
-  if (h->ctrl_host[CW_ERR_INDEX] != 0u) rc = MLA_E_INDEX;
-  return rc;
+  return h->ctrl_host[CW_ERR_INDEX] != 0u ? MLA_E_INDEX : MLA_OK;
 }
 
 // ---- panel (standalone lu_blk_ll) --------------------------------------------------------------------
@@ -449,7 +382,10 @@ static int check_abort(mla_handle h, cudaStream_t s) {
     return MLA_E_CUDA;
   cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) { h->last_cuda = (int)e; return MLA_E_CUDA; }
-  return h->ctrl_host[CW_ABORT] != 0u ? MLA_E_ABORT : MLA_OK;
+  if (h->ctrl_host[CW_ABORT] == 0u) return MLA_OK;
+  // an aborted panel team leaves its exchange slots / sequence number half-way: start the next one clean
+  cudaMemsetAsync(h->panel_ws, 0, sizeof(PanelWs), s);
+  return MLA_E_ABORT;
 }
 
 extern "C" int mla_panel_ll(mla_handle h, double* P, int64_t m, int64_t w, int64_t ld, int32_t* ipiv, int b_inner,
@@ -662,6 +598,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
     return TileDesc{a.P + i0, a.ldp, a.T + (int64_t)c0 * a.ldt, a.ldt, c, a.ldt, c, a.ldt,
                     a.w, a.rows - i0, imin(TRSM_CW, a.cols - c0), 1.0, -1.0, true};
   };
+  // a pivot index out of range (k_laswp_plan's verdict): nothing may be touched, and the caller must
+  // hear about it -- the abort word is what the asynchronous entry points report (mla_abort_word)
+  if (*((volatile unsigned*)(a.ctrl + CW_ERR_INDEX)) != 0u) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.ctrl + CW_ABORT, 0xBAD1u);
+    return;
+  }
   int base = 0, ready_strip = -1;
   bool primed = false;
   int t = pop_item(next);
@@ -707,7 +649,7 @@ extern "C" int mla_apply_panel_prepare(mla_handle h, const int32_t* ipiv, int64_
   if (!h || rows < w || w < 0 || w > kMaxPiv) return MLA_E_INVALID;
   if (w == 0) return MLA_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  k_laswp_plan<<<1, 32, 0, s>>>(ipiv, (int)w, rows, 0, h->plan, h->ctrl);
+  k_laswp_plan<<<1, 32, 0, s>>>(ipiv, (int)w, rows, 0, 0, 0, h->plan, h->ctrl);
   CK(h, cudaGetLastError());
   CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
   ++h->apply_tag;

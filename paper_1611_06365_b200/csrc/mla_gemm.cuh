@@ -42,7 +42,6 @@ struct GemmCfg {
 };
 
 using GemmUpdateCfg = GemmCfg<128, 128, 2, 4, 3, 32>;  // trailing update tiles
-using GemmHalfCfg = GemmCfg<128, 64, 2, 2, 2, 32, 128>;   // experiment: 128-thread CTAs, two per SM
 using GemmPanelCfg = GemmCfg<128, 32, 8, 1, 4>;    // panel-internal update (N = inner block)
 using GemmPanel16Cfg = GemmCfg<128, 16, 8, 1, 4>;  // same, for blocks narrowed to 16 columns (slab fitting)
 using GemmPanel8Cfg = GemmCfg<128, 8, 8, 1, 4>;    // ... and to 8 columns (very tall panels)
@@ -306,6 +305,9 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
       // slot this tile consumed last, and added into C by one 1-KiB bulk reduction per column.
       double* stg = smem + ((base + KT - 1) % STAGES) * Cfg::STAGE;
       static_assert(64 * RED_LDS <= Cfg::STAGE, "staging fits one ring slot");
+      // that slot is the one the k loop's LAST iteration read its fragments from: every warp must be
+      // through with them before the first staging store lands there
+      grp_sync<Cfg::THREADS>();
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         if ((wj >> 1) == half) {

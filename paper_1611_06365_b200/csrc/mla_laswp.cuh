@@ -40,16 +40,22 @@ struct PivPlan {           // global-memory storage of one full-size plan
 // step; validation and the final compaction are warp-parallel.
 // Returns false (and count = 0) if an index is out of range -- nothing may then be touched
 // (kernels.py:326-327).
+// t0 > 0: the block is chunk [t0, t0+npiv) of a longer pivot vector of the same view: interchange s of
+// the chunk swaps view rows t0+s and ipiv[s], and ipiv[s] may lie anywhere in [0, rows) -- above the
+// chunk as well (the reference's laswp accepts any in-range index, kernels.py:316-327).  Row ids in
+// the plan are view rows; "top" rows are [t0, t0+npiv), every other touched row goes through the hash.
 __device__ inline bool build_pivot_plan(const int* ipiv, int npiv, int64_t rows, bool reverse,
-                                        PlanRef plan, int* top, int* keys, int* vals, int tsize, int* pv) {
+                                        PlanRef plan, int* top, int* keys, int* vals, int tsize, int* pv,
+                                        int t0 = 0) {
   const int lane = threadIdx.x & 31;
   bool bad = false;
   for (int t = lane; t < npiv && t < kMaxPiv; t += 32) {
     int p = ipiv[t];
     if (p < 0 || (int64_t)p >= rows) bad = true;
-    top[t] = t;
+    top[t] = t0 + t;
     pv[t] = p;
   }
+  if ((int64_t)t0 + npiv > rows) bad = true;
   for (int x = lane; x < tsize; x += 32) keys[x] = -1;
   bad = __any_sync(0xffffffffu, bad);
   if (bad || npiv > kMaxPiv || tsize < 2 * npiv) {
@@ -63,9 +69,10 @@ __device__ inline bool build_pivot_plan(const int* ipiv, int npiv, int64_t rows,
     for (int s = 0; s < npiv; ++s) {
       const int t = reverse ? (npiv - 1 - s) : s;
       const int p = pv[t];
-      if (p == t) continue;
-      if (p < npiv) {
-        int a = top[t]; top[t] = top[p]; top[p] = a;
+      const int pl = p - t0;
+      if (pl == t) continue;
+      if (pl >= 0 && pl < npiv) {
+        int a = top[t]; top[t] = top[pl]; top[pl] = a;
       } else {
         unsigned h = ((unsigned)p * 2654435761u) & mask;
         while (true) {
@@ -85,15 +92,16 @@ __device__ inline bool build_pivot_plan(const int* ipiv, int npiv, int64_t rows,
   for (int t = lane; t < npiv; t += 32) pv[t] = -1;
   __syncwarp();
   for (int x = lane; x < tsize; x += 32)
-    if (keys[x] >= 0 && vals[x] < npiv) pv[vals[x]] = keys[x];   // each source row occurs once
+    if (keys[x] >= 0 && vals[x] >= t0 && vals[x] < t0 + npiv) pv[vals[x] - t0] = keys[x];   // each source row occurs once
   __syncwarp();
   int cnt = 0;
   for (int base = 0; base < 2 * npiv + tsize; base += 32) {
     int e = base + lane;
     int d = -1, sidx = -1;
-    if (e < npiv) { d = e; sidx = top[e]; }
-    else if (e < 2 * npiv) { d = pv[e - npiv]; sidx = e - npiv; }
-    else if (e < 2 * npiv + tsize && keys[e - 2 * npiv] >= 0 && vals[e - 2 * npiv] >= npiv) {
+    if (e < npiv) { d = t0 + e; sidx = top[e]; }
+    else if (e < 2 * npiv) { d = pv[e - npiv]; sidx = t0 + (e - npiv); }
+    else if (e < 2 * npiv + tsize && keys[e - 2 * npiv] >= 0 &&
+             (vals[e - 2 * npiv] < t0 || vals[e - 2 * npiv] >= t0 + npiv)) {
       d = keys[e - 2 * npiv]; sidx = vals[e - 2 * npiv];
     }
     bool keep = (d >= 0) && (d != sidx);

@@ -37,7 +37,7 @@ CONFIGS = {
     "config1": LuConfig("config1", 2048, "uniform", 0, 256, 32),
     "config2": LuConfig("config2", 8192, "normal", 1, 256, 32),
     "config3": LuConfig("config3", 16384, "uniform_rowscaled", 2, 512, 64),
-    "config4": LuConfig("config4", 32768, "normal", 3, 256, 32),
+    "config4": LuConfig("config4", 32768, "normal", 3, 512, 64),   # headline point of the b sweep {128,256,512,768}, b_i = b/8
     "config5": LuConfig("config5", 65536, "uniform", 4, 512, 64),
 }
 

@@ -5,7 +5,9 @@
 Produced with the C oracle (bit-pinned to the reference by tests/test_oracle_golden.py); with
 --reference the unmodified reference also runs (n <= 8192 is practical: ~2 min) and the two packed
 factor arrays are required to be bitwise identical before anything is written.  Stored per config:
-int32 pivots, sha256 of the packed factors, the diagonal of U, and the residual.
+int32 pivots, sha256 of the packed factors, the diagonal of U and -- for check (b) of north_star at
+sizes where the GPU test cannot afford a full oracle run -- SAMPLE_K full rows and SAMPLE_K full columns
+of the packed factors together with every column's max |entry| (the scale of the 1e-10 bound).
 """
 from __future__ import annotations
 
@@ -21,6 +23,17 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 import oracle  # noqa: E402
 from paper_1611_06365_b200.workloads import CONFIGS, make_config_matrix  # noqa: E402
+
+
+SAMPLE_K = 8
+
+
+def sample_indices(n: int, k: int = SAMPLE_K) -> np.ndarray:
+    """k row/column indices spread over [0, n): both ends, and interior points that are NOT multiples of
+    the block sizes (odd offsets), so panel interiors, panel edges and the last rows are all hit."""
+    base = np.linspace(0, n - 1, k).astype(np.int64)
+    base[1:-1] += 37
+    return np.unique(np.clip(base, 0, n - 1))
 
 
 def main():
@@ -43,9 +56,12 @@ def main():
         assert np.array_equal(a, b), "oracle factors differ from the reference"
         print("oracle == reference bitwise at n =", cfg.n)
     sha = hashlib.sha256(a.tobytes(order="F")).digest()
+    idx = sample_indices(cfg.n)
     np.savez_compressed(os.path.join(HERE, f"golden_{name}.npz"),
                         ipiv=r.ipiv.astype(np.int32), sha=np.frombuffer(sha, dtype=np.uint8),
                         diag=np.array(np.diag(a)), b_outer=cfg.b_outer, b_inner=cfg.b_inner,
+                        sample_idx=idx, sample_rows=np.ascontiguousarray(a[idx, :]),
+                        sample_cols=np.ascontiguousarray(a[:, idx]), colmax=np.abs(a).max(axis=0),
                         pinned_by=np.array(["reference+oracle" if "--reference" in sys.argv else "oracle"]))
     print("wrote", name)
 

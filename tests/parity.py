@@ -38,3 +38,16 @@ def assert_parity(got_lu, got_ipiv, ref_lu, ref_ipiv, what=""):
     err, strict = lu_error(got_lu, ref_lu)
     assert err <= LU_RTOL, f"{what}: factors differ by {err:.3e} (column-scaled), strict {strict:.3e}"
     return err, strict
+
+
+def sampled_lu_error(got_rows, got_cols, g):
+    """Check (b) on the sampled rows / columns of a full-size fixture (tests/golden/make_golden_big.py,
+    make_golden_lapack.py): same column-scaled relative error as lu_error, the scale being
+    max(|ref_ij|, max_i |ref_ij|) with the column maxima stored in the fixture."""
+    idx, colmax = g["sample_idx"], g["colmax"]
+    ref_rows, ref_cols = g["sample_rows"], g["sample_cols"]
+    sr = np.maximum(np.abs(ref_rows), colmax[None, :])
+    sc = np.maximum(np.abs(ref_cols), colmax[idx][None, :])
+    sr[sr == 0.0] = 1.0
+    sc[sc == 0.0] = 1.0
+    return max(float((np.abs(got_rows - ref_rows) / sr).max()), float((np.abs(got_cols - ref_cols) / sc).max()))

@@ -126,6 +126,46 @@ def test_config_shaped_bitwise(golden, c):
     assert oracle.residual_lu(a0, a, r.ipiv) <= n * 100 * np.finfo(np.float64).eps
 
 
+@pytest.mark.parametrize("c", cases.BIG, ids=lambda c: c["name"])
+def test_lapack_pivots_equal_the_pinned_oracle(golden, c):
+    """LAPACK getrf is the second oracle for config 5 (n = 65536: no reference run is affordable,
+    SURVEY.md 8c; tests/golden/make_golden_lapack.py).  Before its fixture is trusted: on the
+    config-1/2/3 shaped inputs its pivot vector equals the REFERENCE-produced golden pivots and its
+    factors agree with the pinned oracle's to the parity bound."""
+    scipy_linalg = pytest.importorskip("scipy.linalg")
+    from parity import lu_error
+    a = np.asfortranarray(make_matrix(c["dist"], c["n"], c["seed"]))
+    ref = a.copy(order="F")
+    oracle.lu_la(ref, c["b_o"], c["b_i"])
+    lu, piv = scipy_linalg.lu_factor(a, overwrite_a=True, check_finite=False)
+    assert np.array_equal(piv.astype(np.int32), golden[c["name"] + "/ipiv"])
+    err, _ = lu_error(lu, ref)
+    assert err <= 1e-10
+
+
+def test_full_size_fixtures_are_consistent():
+    """golden_config{2..5}.npz: pivots are valid LAPACK-style interchanges (ipiv[k] >= k, < n), diag(U)
+    has no zero, and -- where sampled rows / columns are stored -- they agree with diag and colmax."""
+    import os
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    for name in ("config2", "config3", "config4", "config5"):
+        path = os.path.join(here, f"golden_{name}.npz")
+        if not os.path.exists(path):
+            continue
+        g = np.load(path)
+        piv, n = g["ipiv"].astype(np.int64), g["ipiv"].shape[0]
+        assert np.all(piv >= np.arange(n)) and np.all(piv < n)
+        assert np.all(g["diag"] != 0.0)
+        if "sample_idx" in g.files:
+            idx = g["sample_idx"]
+            rows, cols = g["sample_rows"], g["sample_cols"]
+            assert rows.shape == (idx.size, n) and cols.shape == (n, idx.size)
+            assert np.array_equal(rows[np.arange(idx.size), idx], g["diag"][idx])
+            assert np.array_equal(cols[idx, np.arange(idx.size)], g["diag"][idx])
+            assert np.array_equal(rows[:, idx], cols[idx, :])
+            assert np.all(np.abs(rows) <= g["colmax"][None, :]) and np.all(np.abs(cols) <= g["colmax"][idx][None, :])
+
+
 # ---- the reference's own known-answer tests, restated on the oracle --------------------------
 
 def test_kat_1x1_and_permutation():  # test_lu.py:29-42
