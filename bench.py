@@ -5,12 +5,17 @@
                     [--config config4] [--n N] [--variant lu_et] [--b-outer B] [--b-inner b]
 
 One "step" = one whole factorization of the config's synthetic matrix (seeded).
-N=1 default workload: config4 (n=32768, N(0,1) seed 3, b=256/32) -- the configuration the target is
-quoted on.  N>1: config5 (n=65536, 1-D block-cyclic columns, NCCL panel broadcast).  Rank 0 prints
-ONE JSON line.  `value` is timed with CUDA events around the factorization only (inputs resident in
-HBM, restored from a pristine device copy between steps, outside the timed region); `e2e` times the
-C-ABI call with host buffers (H2D + factor + D2H inside).  `--impl reference` times the CPU oracle
-port (oracle/, bit-identical to the reference package) on the host cores.
+N=1 default workload: config4 (n=32768, N(0,1) seed 3) at b=512/64 -- the best point of config 4's block
+sweep b in {128,256,512,768}, b_i = b/8, and the configuration the >= 60 % target is quoted on.  N>1:
+config5 (n=65536, b=512/64, 1-D block-cyclic columns, NCCL panel broadcast, look-ahead + WS + ET per GPU).
+Rank 0 prints ONE JSON line.  `value` is timed with CUDA events around the factorization only (inputs
+resident in HBM, restored from a pristine device copy between steps, outside the timed region); `e2e` is
+the mean of 5 timed calls of the C-ABI entry point with pinned host buffers (H2D + factor + D2H inside).
+`--impl reference` times the CPU oracle port (oracle/, bit-identical to the reference package, which is
+Python + numba and cannot travel to the GPU box) on all host cores: its `config` is this arm's, each step
+is a BOUNDED SAMPLE of that workload (the leading n_s x n_s block of the same matrix, n_s chosen so the
+run ends within a few minutes and printed as `sample_n`), next to a measured n-curve and the explicit
+projection to the full size.
 """
 from __future__ import annotations
 
@@ -35,6 +40,8 @@ from paper_1611_06365_b200.workloads import CONFIGS, flops_lu, make_matrix  # no
 # per iteration) is 2 * 8 * n^3 / (3 b) = 367 GB at b = 512 (ET cuts make the effective b smaller).
 # At b=256/32 the same measurement gave 577.2 + 423.0 GB against a minimum of 733 GB.
 DEFAULT_WORKLOAD_DRAM_BYTES = 493252247808 + 229810838016
+DEFAULT_WORKLOAD_DRAM_SOURCE = ("profiles/r01_getrf_n32768_traffic.csv (ncu dram__bytes_read.sum + dram__bytes_write.sum of "
+                                "the k_getrf launch of this same command, captured in a separate run under ncu)")
 
 FP64_TENSOR_PEAK_TFLOPS = 37.0   # measured on this pool's B200: tools/fp64_peak.cu (DMMA.8x8x4
                                  # issue-bound, 3 s sustained) -> profiles/r01_fp64_peak.log.
@@ -165,32 +172,54 @@ def pick(args, world):
     return name, cfg, n, b_o, b_i
 
 
+def workload_config(name, cfg, n, b_o, b_i, variant, sm_pf, world):
+    """The `config` object of the JSON line -- identical for both arms (the reference arm times a bounded
+    sample OF THIS workload and says so in `sample_n` / `cpu_baseline.sample`)."""
+    c = {"workload": f"{name}: LU n={n} b={b_o}/{b_i} {cfg.dist} seed {cfg.seed}", "variant": variant,
+         "l2": "inputs larger than L2 (8 B * n^2) and restored from a pristine copy between steps"}
+    if world == 1:
+        c["sm_pf"] = sm_pf
+    else:
+        c["layout"] = "1-D block-cyclic columns, NCCL panel+pivot broadcast, look-ahead+WS+ET per GPU"
+    return c
+
+
+_MATRIX_CACHE = {}
+
+
 def cpu_oracle_run(cfg, n, b_o, b_i, threads=None):
-    """Time the CPU oracle port (bit-identical to the reference) on an n x n instance of cfg."""
+    """Time the CPU oracle port (bit-identical to the reference) on the leading n x n block of cfg's
+    generator family (same distribution and seed)."""
     import oracle
     if threads:
         oracle.set_num_threads(threads)
-    a = np.asfortranarray(make_matrix(cfg.dist, n, cfg.seed))
+    key = (cfg.dist, cfg.seed, n)
+    if key not in _MATRIX_CACHE:
+        _MATRIX_CACHE.clear()
+        _MATRIX_CACHE[key] = np.asfortranarray(make_matrix(cfg.dist, n, cfg.seed))
+    a = _MATRIX_CACHE[key].copy(order="F")
     t0 = time.perf_counter()
     oracle.lu_la(a, b_o, b_i)
     dt = time.perf_counter() - t0
     return flops_lu(n, n) / dt / 1e9, dt, oracle.num_threads()
 
 
+SAMPLE_SIZES = (16384, 12288, 8192, 6144, 4096, 3072, 2048)
+
+
 def cpu_baseline(cfg, b_o, b_i, budget_s=15.0):
-    """Bounded sample: probe at n=1536, then the largest n (multiple of 512, <= 8192) whose
-    predicted time fits the budget."""
+    """Bounded sample: probe at n=1536, then the largest n (<= 16384) whose predicted time fits the budget."""
     gf, dt, cores = cpu_oracle_run(cfg, 1536, b_o, b_i)
     n = 1536
-    for cand in (8192, 6144, 4096, 3072, 2048):
+    for cand in SAMPLE_SIZES:
         if flops_lu(cand, cand) / (gf * 1.5e9) <= budget_s:   # rate improves with n
             n = cand
             break
     if n > 1536:
         gf, dt, cores = cpu_oracle_run(cfg, n, b_o, b_i)
     return {"value": round(gf, 3), "unit": "GFLOP/s", "cores": cores, "kind": "port",
-            "sample": f"oracle lu_la on the {cfg.dist} seed-{cfg.seed} matrix truncated to n={n}, "
-                      f"b={b_o}/{b_i}, {dt:.1f} s (full n would be projected, not run)"}
+            "sample": f"oracle lu_la on the {cfg.dist} seed-{cfg.seed} matrix at n={n}, "
+                      f"b={b_o}/{b_i}, {dt:.1f} s (bounded sample; the full n is projected, not run)"}
 
 
 def run_reference(args):
@@ -200,12 +229,18 @@ def run_reference(args):
     name, cfg, n_full, b_o, b_i = pick(args, args.gpus)
     import oracle
     cores = oracle.num_threads()
-    # bounded sample sized from a probe so K+W steps end within a few minutes
-    gf, dt, _ = cpu_oracle_run(cfg, 1536, b_o, b_i)
+    # measured n-curve (one run each): shows the CPU rate is flat in n, which is what the projection to
+    # the full size rests on
+    curve = {}
+    for nn in (min(2048, n_full), min(4096, n_full)):
+        gf, dt, _ = cpu_oracle_run(cfg, nn, b_o, b_i)
+        curve[str(nn)] = {"gflops": round(gf, 2), "seconds": round(dt, 2)}
+    gf = curve[str(min(4096, n_full))]["gflops"]
+    # the bounded sample: the largest size whose K+W steps end within ~4 minutes at the measured rate
     total = max(1, args.steps + args.warmup)
-    n = 1536
-    for cand in (8192, 6144, 4096, 3072, 2048):
-        if total * flops_lu(cand, cand) / (gf * 1.5e9) <= 150.0:
+    n = min(2048, n_full)
+    for cand in SAMPLE_SIZES:
+        if cand <= n_full and total * flops_lu(cand, cand) / (gf * 1e9) <= 240.0:
             n = cand
             break
     for _ in range(args.warmup):
@@ -216,13 +251,20 @@ def run_reference(args):
         times.append(dt)
     dt = sum(times) / len(times)
     val = flops_lu(n, n) / dt / 1e9
+    curve[str(n)] = {"gflops": round(val, 2), "seconds": round(dt, 2)}
+    proj_s = flops_lu(n_full, n_full) / (val * 1e9)
     sample = (f"oracle port of the reference lu_la (bit-identical, tests/test_oracle_golden.py) on the "
-              f"{cfg.dist} seed-{cfg.seed} matrix truncated to n={n}, b={b_o}/{b_i}, all {cores} host threads")
+              f"{cfg.dist} seed-{cfg.seed} matrix at n={n} (bounded sample of the n={n_full} workload), "
+              f"b={b_o}/{b_i}, all {cores} host threads; projected full-size step at this rate: {proj_s:.0f} s")
+    t_pf = 32 if args.sm_pf is None else args.sm_pf
     print(json.dumps({
         "impl": "reference", "metric": "LU GFLOP/s (2n^3/3 / time)", "value": round(val, 3), "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{name}: LU n={n_full} b={b_o}/{b_i} {cfg.dist} seed {cfg.seed}", "sample_n": n},
+        "config": workload_config(name, cfg, n_full, b_o, b_i, args.variant, t_pf, args.gpus),
+        "sample_n": n, "n_curve": curve,
+        "projected_full_size": {"n": n_full, "seconds_per_step": round(proj_s, 1), "gflops": round(val, 3),
+                                "basis": "GFLOP/s measured at sample_n; the n-curve shows the rate is flat in n"},
         "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -234,11 +276,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback); use --impl reference for the CPU arm")
+    if args.gpus != world:
+        raise SystemExit(f"bench.py --gpus {args.gpus} must be launched with torchrun --nproc-per-node {args.gpus} "
+                         f"(WORLD_SIZE is {world}); one process per GPU")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py --gpus {world}: only {torch.cuda.device_count()} CUDA device(s) visible on this node")
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py needs a CUDA device (no CPU fallback); use --impl reference for the CPU arm")
     import paper_1611_06365_b200 as mla
     name, cfg, n, b_o, b_i = pick(args, world)
     dev = torch.device("cuda", local)
@@ -249,7 +296,7 @@ def run_ours(args):
 
     if world > 1:
         from paper_1611_06365_b200.distributed import DistLU
-        dlu = DistLU(n, b_o, b_i, cfg, dev, variant=args.variant, pool=pool)
+        dlu = DistLU(n, b_o, b_i, cfg, dev, variant=args.variant if args.variant in DistLU.VARIANTS else "lu_et", pool=pool)
         dlu.generate()
         for _ in range(args.warmup):
             dlu.restore(); dlu.factor()
@@ -293,9 +340,8 @@ def run_ours(args):
                 "metric": "LU GFLOP/s (2n^3/3 / time)", "value": round(val, 1), "unit": "GFLOP/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"{name}: LU n={n} b={b_o}/{b_i} {cfg.dist} seed {cfg.seed}",
-                           "variant": args.variant, "layout": "1-D block-cyclic columns, NCCL panel+pivot broadcast",
-                           "l2": "inputs larger than L2"},
+                "config": workload_config(name, cfg, n, b_o, b_i, args.variant, None, world),
+                "run": {"panels": len(dlu.widths), "et_events": dlu.et_events, "host_waits": dlu.host_waits},
                 "roofline": {"bound": "tensor", "achieved": round(val / 1e3, 3), "peak": FP64_TENSOR_PEAK_TFLOPS * world,
                              "unit": "TFLOP/s", "frac": round(val / 1e3 / (FP64_TENSOR_PEAK_TFLOPS * world), 4),
                              "traffic": None, "peak_source": "measured DMMA issue rate x n_gpus (tools/fp64_peak.cu)"},
@@ -366,7 +412,7 @@ def run_ours(args):
         info = _capi.LuInfo()
         t_pf = pool.t_pf if args.sm_pf is None else args.sm_pf
         e_times = []
-        for i in range(2):
+        for i in range(6):                 # one warm-up call (allocates the cached device buffers) + 5 timed
             work.copy_(host_t)
             t0 = time.perf_counter()
             rc = _capi.lib().mla_getrf_la_host(pool.handle, work.data_ptr(), n, n, n, ipiv_h.data_ptr(), b_o, b_i,
@@ -377,7 +423,8 @@ def run_ours(args):
                 e_times.append(dt)
         e = sum(e_times) / len(e_times)
         e2e = {"value": round(flops / e / 1e9, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n * n,
-               "d2h_bytes_per_step": 8 * n * n + 4 * n, "ms_per_step": round(e * 1e3, 2),
+               "d2h_bytes_per_step": 8 * n * n + 4 * n, "ms_per_step": round(e * 1e3, 2), "timed_calls": len(e_times),
+               "ms_min_max": [round(min(e_times) * 1e3, 2), round(max(e_times) * 1e3, 2)],
                "api": "mla_getrf_la_host (C ABI, pinned host buffers)"}
 
     cpu = None if args.no_cpu else cpu_baseline(cfg, b_o, b_i)
@@ -385,15 +432,14 @@ def run_ours(args):
         "metric": "LU GFLOP/s (2n^3/3 / time)", "value": round(val, 1), "unit": "GFLOP/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{name}: LU n={n} b={b_o}/{b_i} {cfg.dist} seed {cfg.seed}",
-                   "variant": args.variant, "sm_pf": pool.t_pf if args.sm_pf is None else args.sm_pf,
-                   "l2": "inputs larger than L2 (8 B * n^2) and restored from a pristine copy between steps",
-                   "et_events": res.et_events, "ws_joins": res.ws_joins, "panels": len(res.widths),
-                   "gen_seconds": round(gen_s, 1)},
+        "config": workload_config(name, cfg, n, b_o, b_i, args.variant, pool.t_pf if args.sm_pf is None else args.sm_pf, 1),
+        "run": {"et_events": res.et_events, "ws_joins": res.ws_joins, "panels": len(res.widths),
+                "gen_seconds": round(gen_s, 1)},
         "roofline": {"bound": "tensor", "achieved": round(val / 1e3, 3), "peak": FP64_TENSOR_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": round(val / 1e3 / FP64_TENSOR_PEAK_TFLOPS, 4),
                      "traffic": DEFAULT_WORKLOAD_DRAM_BYTES if (name == "config4" and n == 32768 and b_o == 512
                                                                 and args.variant == "lu_et") else None,
+                     "traffic_source": DEFAULT_WORKLOAD_DRAM_SOURCE,
                      "kernel": "k_getrf (persistent; algorithmic flops 2n^3/3 per launch)",
                      "peak_source": "measured: DMMA.8x8x4 issue-bound rate, tools/fp64_peak.cu, "
                                     "profiles/r01_fp64_peak.log (MEASURED_PEAKS.json has no FP64 entry)"},

@@ -82,9 +82,11 @@ int mla_trsm_llu(mla_handle h, const double* L, int64_t w, int64_t ldl, double* 
                  int64_t ldb, void* stream);
 
 /* laswp(a, piv, reverse) -- kernels.py:296-332.  Interchange t <-> ipiv[t] on every column of the
- * rows x cols view, ascending (descending when reverse).  ipiv is a DEVICE int32 array; range
- * validation happens on the device before anything is touched: on a bad index nothing is modified
- * and the (synchronous) return value is MLA_E_INDEX. */
+ * rows x cols view, ascending (descending when reverse).  ipiv is a DEVICE int32 array of any length
+ * npiv <= rows, every entry anywhere in [0, rows) (also above its own position, like the reference);
+ * vectors longer than 1024 are applied in chunks of 1024 inside the call.  The whole vector is
+ * range-checked on the device before anything is touched: on a bad index NOTHING is modified and the
+ * (synchronous) return value is MLA_E_INDEX. */
 int mla_laswp(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
               int64_t npiv, int reverse, void* stream);
 
@@ -103,11 +105,16 @@ int mla_panel_ll(mla_handle h, double* P, int64_t m, int64_t w, int64_t ld, int3
                  const uint32_t* stop_flag, int stop_after_polls, int team_ctas, mla_lu_info* info,
                  void* stream);
 
-/* Asynchronous form for stream-ordered drivers (distributed.py): no stop flag, pivots stay on the
- * device, nothing is read back; singular_accum (device int32, nullable) is OR-ed with the panel's
- * singular flag. */
+/* Asynchronous form for stream-ordered drivers (distributed.py): pivots stay on the device, nothing is
+ * read back; the factored width / singular flag stay in the handle's device-side info record (read by
+ * mla_pack_panel); singular_accum (device int32, nullable) is OR-ed with the panel's singular flag.
+ * stop_flag (device word, nullable) is the ET flag of lu.py:177-179: the panel is cut after a finished
+ * inner block, while columns remain, once *stop_flag == stop_tag (stop_tag == 0: once it is non-zero).
+ * The panel runs in Crout order, so after a cut the leftover columns hold the interchanges and their U
+ * rows (what `pend` records in lu.py:247-255, 324) -- the same contract as the persistent kernel's panels. */
 int mla_panel_ll_async(mla_handle h, double* P, int64_t m, int64_t w, int64_t ld, int32_t* ipiv, int b_inner,
-                       int team_ctas, int32_t* singular_accum, void* stream);
+                       int team_ctas, int32_t* singular_accum, const uint32_t* stop_flag, uint32_t stop_tag,
+                       void* stream);
 
 /* lu_la(a, policy, pool) -- lu.py:197-334.  Whole factorization P*A = L*U in place, one persistent
  * cooperative kernel: SM partition (sm_pf panel CTAs), atomic tile queue, WS and ET by device
@@ -132,11 +139,17 @@ int mla_getrf_la_sync(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld,
                       int b_outer, int b_inner, int variant, int sm_pf, int q_chunks,
                       mla_lu_info* info_host, int32_t* widths_host, int widths_cap, void* stream);
 
+/* Releases the device matrix / pivot buffers mla_getrf_la_host keeps cached in the handle. */
+int mla_release_host_cache(mla_handle h);
+
 /* End-to-end form with HOST buffers (what bench.py's `e2e` times): uploads A (m x n, ld_host),
  * factors on the device, downloads the packed factors and the pivots.  The download overlaps the
  * factorization: rows above the current panel are final (every later interchange, solve and update
  * touches lower rows only), the kernel reports that row through a mapped host word, and the finished
- * row blocks are copied out on a second stream while the kernel is still running.  Synchronous. */
+ * row blocks are copied out on a second stream while the kernel is still running.  Synchronous: the
+ * calling thread polls that word (50 us sleeps) and issues the copies.  The device copy of the matrix
+ * (8 * m * n bytes, e.g. 8 GiB at n = 32768) and the pivot buffer stay cached in the handle for the next
+ * call of the same or a smaller size, until mla_release_host_cache or mla_destroy. */
 int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_t ld_host,
                       int32_t* ipiv_host, int b_outer, int b_inner, int variant, int sm_pf,
                       int q_chunks, mla_lu_info* info_host);
@@ -150,21 +163,41 @@ int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int64_t w, int6
                     int64_t cols, int64_t ldt, const int32_t* ipiv, void* stream);
 
 /* The two halves of mla_apply_panel.  prepare: interchange plan of the w pivots, empty work queue, fresh
- * flag tag.  launch: `ctas` CTAs (0 = mla_set_update_sms / all) draining the prepared queue; a second
+ * step tag.  launch: `ctas` CTAs (0 = mla_set_update_sms / all) draining the prepared queue; a second
  * launch of the same step on another stream JOINS that queue (worker sharing across kernels: the SMs that
- * factored the next panel help with the update once the panel is done). */
+ * factored the next panel help with the update once the panel is done, pool.py:377-414).
+ *   skip_cols: leading columns of T that already carry the interchanges and their U rows (leftover of an
+ *              ET-cut panel, lu.py:247-255): they only take part in the rank-w update;
+ *   L / left_cols / ldl: the owned columns LEFT of the panel (view starting at the panel's first row,
+ *              nullable): they receive the interchanges only (lu.py:252, 329-332), as extra queue items.
+ * The CTA that completes the step's last item publishes the step tag in the handle's step flag
+ * (mla_step_flag) -- the ru_done of lu.py:309-310 for a panel kernel running beside the update. */
 int mla_apply_panel_prepare(mla_handle h, const int32_t* ipiv, int64_t w, int64_t rows, void* stream);
 int mla_apply_panel_launch(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
-                           int64_t cols, int64_t ldt, int ctas, void* stream);
+                           int64_t cols, int64_t ldt, int64_t skip_cols, double* L, int64_t left_cols, int64_t ldl,
+                           int ctas, void* stream);
+
+/* Device address of the handle's step flag and the tag of the step prepared last (mla_apply_panel_prepare):
+ * *flag == tag  <=>  that step's queue has been drained.  Pass both to mla_panel_ll_async as the ET flag. */
+int mla_step_flag(mla_handle h, uint32_t** flag_dev, uint32_t* tag);
+
+/* Pack a factored panel for the broadcast of the multi-GPU driver: out receives
+ *   [int32 x 4: factored width, singular flag, scheduled width w, rows][int32 x w panel-local pivots, padded
+ *    to a multiple of 4][rows x w doubles, column-major, leading dimension rows]
+ * = mla_packed_panel_doubles(rows, w) doubles.  use_panel_info != 0 takes the factored width and the
+ * singular flag from the info record the last panel kernel of THIS handle left on the device (the chain
+ * panel -> pack -> broadcast needs no host read-back); else they are w and 0.  Pivots travel as int32. */
+int mla_pack_panel(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ld, const int32_t* ipiv,
+                   int use_panel_info, double* out, void* stream);
+int64_t mla_packed_panel_doubles(int64_t rows, int64_t w);
 
 /* The device-side abort word of the handle (0 = no watchdog / protocol abort since the last launch that
  * reset it); the asynchronous entry points never read it back themselves.  Synchronises the device. */
 int mla_abort_word(mla_handle h);
 
 /* Number of SMs mla_apply_panel launches on (0 = all).  Lets a multi-GPU driver leave SMs to the
- * communication kernels or to another kernel of its own.  (Running mla_panel_ll_async beside an update
- * this way is what distributed.py's experimental two-stream mode does; that mode currently races and
- * is off by default.) */
+ * communication kernels or to the look-ahead panel (mla_panel_ll_async on another stream and another
+ * handle) that runs beside the update. */
 int mla_set_update_sms(mla_handle h, int ctas);
 
 /* fill_random(a, seed) -- matrix.py:44-63: SplitMix64 stream, bit-identical to the reference;

@@ -56,6 +56,9 @@ def lib() -> ctypes.CDLL:
         L.orc_lu_la.argtypes = [_dp, _i64, _i64, _i64, _i64, _i64, _ip, _ip, _i64,
                                 ctypes.POINTER(ctypes.c_int), _ip, _i64, _ip, _i64]
         L.orc_lu_la.restype = _i64
+        L.orc_lu_la_clamped.argtypes = [_dp, _i64, _i64, _i64, _i64, _i64, _ip, _ip, _i64,
+                                        ctypes.POINTER(ctypes.c_int), _ip, _i64, _ip, _i64, _i64]
+        L.orc_lu_la_clamped.restype = _i64
         L.orc_residual_lu.argtypes = [_dp, _dp, _i64, _i64, _i64, _i64, _ip]
         L.orc_residual_lu.restype = ctypes.c_double
         _lib = L
@@ -167,8 +170,9 @@ def lu_blk_rl(a: np.ndarray, b: int, inner_b: int | None = None, k_c: int = 256)
     return OracleResult(ipiv, n, bool(sing.value))
 
 
-def lu_la(a: np.ndarray, b_outer: int, b_inner: int, et_sched=None, k_c: int = 256) -> OracleResult:
-    """Serial restatement of lu_la (any non-ET variant); et_sched replays an ET cut schedule."""
+def lu_la(a: np.ndarray, b_outer: int, b_inner: int, et_sched=None, k_c: int = 256, clamp: int = 0) -> OracleResult:
+    """Serial restatement of lu_la (any non-ET variant); et_sched replays an ET cut schedule.
+    clamp > 0: panels never cross a multiple of `clamp` columns (the multi-GPU driver's schedule)."""
     p, m, n, ld = _mat(a)
     if m < n:
         raise ValueError("need m >= n")
@@ -182,8 +186,8 @@ def lu_la(a: np.ndarray, b_outer: int, b_inner: int, et_sched=None, k_c: int = 2
     else:
         sched = np.ascontiguousarray(et_sched, dtype=np.int64)
         sp, ns = _piv(sched), sched.shape[0]
-    ev = lib().orc_lu_la(p, m, n, ld, b_outer, b_inner, _piv(ipiv), sp, ns, ctypes.byref(sing),
-                         _piv(widths), cap, _piv(nw), k_c)
+    ev = lib().orc_lu_la_clamped(p, m, n, ld, b_outer, b_inner, _piv(ipiv), sp, ns, ctypes.byref(sing),
+                                 _piv(widths), cap, _piv(nw), k_c, int(clamp))
     return OracleResult(ipiv, n, bool(sing.value), int(ev), tuple(int(x) for x in widths[:int(nw[0])]))
 
 

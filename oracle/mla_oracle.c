@@ -271,15 +271,33 @@ void orc_lu_blk_rl(double *a, int64_t m, int64_t n, int64_t ld, int64_t b, int64
  * columns already carry the swaps.  widths_out (optional, capacity widths_cap) receives every
  * panel's factored width in order (prologue first); *n_widths the count.
  * ipiv is global, 0-based (lu.py:236, 317).  Returns the number of ET events. */
+int64_t orc_lu_la_clamped(double *a, int64_t m, int64_t n, int64_t ld, int64_t b_o, int64_t b_i,
+                          int64_t *ipiv, const int64_t *et_sched, int64_t n_sched, int *singular,
+                          int64_t *widths_out, int64_t widths_cap, int64_t *n_widths, int64_t k_c,
+                          int64_t clamp);
+
 int64_t orc_lu_la(double *a, int64_t m, int64_t n, int64_t ld, int64_t b_o, int64_t b_i,
                   int64_t *ipiv, const int64_t *et_sched, int64_t n_sched, int *singular,
                   int64_t *widths_out, int64_t widths_cap, int64_t *n_widths, int64_t k_c) {
+  return orc_lu_la_clamped(a, m, n, ld, b_o, b_i, ipiv, et_sched, n_sched, singular, widths_out,
+                           widths_cap, n_widths, k_c, 0);
+}
+
+/* clamp > 0: the panel schedule of the 1-D block-cyclic multi-GPU layout (this spec's design, SURVEY.md
+ * 8e; the reference has no multi-device path): a panel never crosses a multiple of `clamp` columns
+ * (the column block = the unit of ownership), everything else -- operators, order, ET bookkeeping -- is
+ * lu.py:224-332 unchanged.  clamp == 0 is the reference's schedule. */
+int64_t orc_lu_la_clamped(double *a, int64_t m, int64_t n, int64_t ld, int64_t b_o, int64_t b_i,
+                          int64_t *ipiv, const int64_t *et_sched, int64_t n_sched, int *singular,
+                          int64_t *widths_out, int64_t widths_cap, int64_t *n_widths, int64_t k_c,
+                          int64_t clamp) {
   int64_t et_events = 0, nw = 0;
   *singular = 0;
   if (n_widths) *n_widths = 0;
   if (n == 0) return 0;
   int64_t *piv_local = (int64_t *)malloc(sizeof(int64_t) * (size_t)(b_o > 0 ? b_o : 1));
   int64_t w0 = b_o < n ? b_o : n;
+  if (clamp > 0 && w0 > clamp) w0 = clamp;
   orc_lu_blk_ll(a, m, w0, ld, b_i, piv_local, 0, singular, k_c);
   for (int64_t t = 0; t < w0; ++t) ipiv[t] = piv_local[t];
   if (widths_out && nw < widths_cap) widths_out[nw] = w0;
@@ -288,6 +306,7 @@ int64_t orc_lu_la(double *a, int64_t m, int64_t n, int64_t ld, int64_t b_o, int6
   while (q1 < n) {
     ++it;
     int64_t w = b_target < n - q1 ? b_target : n - q1;
+    if (clamp > 0 && w > clamp - q1 % clamp) w = clamp - q1 % clamp;
     /* sync_task, lu.py:251-255 */
     orc_laswp(&A_(a, ld, q0, 0), m - q0, q0, ld, piv_local, npiv_prev, 0);
     orc_laswp(&A_(a, ld, q0, pend), m - q0, n - pend, ld, piv_local, npiv_prev, 0);

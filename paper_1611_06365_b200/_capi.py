@@ -58,12 +58,22 @@ def lib() -> ctypes.CDLL:
     L.mla_getrf_trace.restype = ctypes.c_int
     L.mla_apply_panel.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp]
     L.mla_apply_panel.restype = ctypes.c_int
-    L.mla_panel_ll_async.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, ctypes.c_int, ctypes.c_int, _vp, _vp]
+    L.mla_panel_ll_async.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, ctypes.c_int, ctypes.c_int, _vp, _vp,
+                                     ctypes.c_uint32, _vp]
     L.mla_panel_ll_async.restype = ctypes.c_int
     L.mla_apply_panel_prepare.argtypes = [_vp, _vp, _i64, _i64, _vp]
     L.mla_apply_panel_prepare.restype = ctypes.c_int
-    L.mla_apply_panel_launch.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, ctypes.c_int, _vp]
+    L.mla_apply_panel_launch.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _i64,
+                                         ctypes.c_int, _vp]
     L.mla_apply_panel_launch.restype = ctypes.c_int
+    L.mla_step_flag.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_uint32)]
+    L.mla_step_flag.restype = ctypes.c_int
+    L.mla_pack_panel.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, ctypes.c_int, _vp, _vp]
+    L.mla_pack_panel.restype = ctypes.c_int
+    L.mla_packed_panel_doubles.argtypes = [_i64, _i64]
+    L.mla_packed_panel_doubles.restype = _i64
+    L.mla_release_host_cache.argtypes = [_vp]
+    L.mla_release_host_cache.restype = ctypes.c_int
     L.mla_abort_word.argtypes = [_vp]
     L.mla_abort_word.restype = ctypes.c_int
     L.mla_set_update_sms.argtypes = [_vp, ctypes.c_int]
@@ -86,7 +96,8 @@ EXPORTS = ("mla_version", "mla_create", "mla_destroy", "mla_num_sms", "mla_last_
            "mla_gemm", "mla_trsm_llu", "mla_laswp", "mla_panel_ll", "mla_getrf_la",
            "mla_getrf_la_sync", "mla_getrf_la_host", "mla_fill_random", "mla_panel_profile", "mla_getrf_trace", "mla_laswp_async", "mla_getrf_debug",
            "mla_apply_panel", "mla_set_panel_sms_max", "mla_panel_ll_async",
-           "mla_set_update_sms", "mla_apply_panel_prepare", "mla_apply_panel_launch", "mla_abort_word")
+           "mla_set_update_sms", "mla_apply_panel_prepare", "mla_apply_panel_launch", "mla_abort_word",
+           "mla_step_flag", "mla_pack_panel", "mla_packed_panel_doubles", "mla_release_host_cache")
 
 
 class MlaError(RuntimeError):

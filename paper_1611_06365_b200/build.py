@@ -9,7 +9,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmla_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+# -cudart shared: the library uses the process's libcudart.so.12 (the one torch has already loaded, or the
+# toolkit's through the rpath) instead of embedding a private copy of the whole runtime.
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17", "-shared",
+         "-cudart", "shared", "-Xlinker", "-rpath=/usr/local/cuda/lib64",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--use_fast_math=false"]
 
 

@@ -25,6 +25,8 @@ enum CtrlWord {
   CW_BAR_ALL = 2,
   CW_BAR_PF = 3,
   CW_ERR_INDEX = 4,
+  CW_QUEUE_DONE = 5,   // items of the current apply step completed (all launches of the step)
+  CW_STEP_DONE = 6,    // = the step's tag once its queue has been drained: the distributed driver's ru_done
   CW_COUNT = 64
 };
 
@@ -354,6 +356,9 @@ struct PanelKArgs {
   const unsigned* stop_flag; int stop_after_polls;
   PanelWs* ws; unsigned* ctrl; mla_lu_info* info;
   int* sing_accum;   // nullable: OR-ed with the panel's singular flag (asynchronous callers)
+  unsigned stop_eq;  // 0: the stop flag is "set" when non-zero; else when it equals this tag
+  int crout;         // 1: Crout order even when stoppable (stream-ordered drivers: after a cut the leftover
+                     //    columns carry the interchanges AND their U rows, like the persistent kernel's panels)
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_panel(PanelKArgs a) {
@@ -365,8 +370,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_panel(PanelKArgs a) {
   // left-looking order: after a cut the untouched columns carry the interchanges and nothing else
   // (lu.py:177-179, test_lu.py:132-145).
   const bool stoppable = a.stop_flag != nullptr || a.stop_after_polls > 0;
-  PanelResult r = panel_ll(team, a.P, a.m, a.w, a.ld, a.ipiv, a.b_inner, a.stop_flag, 0u, a.stop_after_polls,
-                           a.ws, smem, kDynSmemDoubles, !stoppable);
+  PanelResult r = panel_ll(team, a.P, a.m, a.w, a.ld, a.ipiv, a.b_inner, a.stop_flag, a.stop_eq, a.stop_after_polls,
+                           a.ws, smem, kDynSmemDoubles, !stoppable || a.crout != 0);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.info->cols_factored = r.cols_factored;
     a.info->singular = r.singular;
@@ -405,7 +410,7 @@ extern "C" int mla_panel_ll(mla_handle h, double* P, int64_t m, int64_t w, int64
   if (grid > kMaxTeam) grid = kMaxTeam;
   CK(h, cudaMemsetAsync(h->ctrl, 0, CW_COUNT * sizeof(unsigned), s));
   PanelKArgs a{P, (int)m, (int)w, ld, ipiv, b_inner, stop_flag, stop_after_polls, h->panel_ws, h->ctrl, h->info_dev,
-               nullptr};
+               nullptr, 0u, 0};
   void* args[] = {&a};
   CK(h, cudaLaunchCooperativeKernel((void*)k_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
   CK(h, cudaMemcpyAsync(h->info_host, h->info_dev, sizeof(mla_lu_info), cudaMemcpyDeviceToHost, s));
@@ -415,7 +420,8 @@ extern "C" int mla_panel_ll(mla_handle h, double* P, int64_t m, int64_t w, int64
 }
 
 extern "C" int mla_panel_ll_async(mla_handle h, double* P, int64_t m, int64_t w, int64_t ld, int32_t* ipiv,
-                                  int b_inner, int team_ctas, int32_t* singular_accum, void* stream) {
+                                  int b_inner, int team_ctas, int32_t* singular_accum, const uint32_t* stop_flag,
+                                  uint32_t stop_tag, void* stream) {
   if (!h || m < w || w < 0 || b_inner < 1 || (m > 0 && ld < m)) return MLA_E_INVALID;
   if (w == 0) return MLA_OK;
   cudaStream_t s = (cudaStream_t)stream;
@@ -428,7 +434,8 @@ extern "C" int mla_panel_ll_async(mla_handle h, double* P, int64_t m, int64_t w,
   if (grid > h->num_sms) grid = h->num_sms;
   if (grid > kMaxTeam) grid = kMaxTeam;
   CK(h, cudaMemsetAsync(h->ctrl, 0, CW_COUNT * sizeof(unsigned), s));
-  PanelKArgs a{P, (int)m, (int)w, ld, ipiv, b_inner, nullptr, 0, h->panel_ws, h->ctrl, h->info_dev, singular_accum};
+  PanelKArgs a{P, (int)m, (int)w, ld, ipiv, b_inner, stop_flag, 0, h->panel_ws, h->ctrl, h->info_dev, singular_accum,
+               stop_tag, 1};
   void* args[] = {&a};
   CK(h, cudaLaunchCooperativeKernel((void*)k_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
   return MLA_OK;
@@ -506,6 +513,13 @@ extern "C" int mla_getrf_la_sync(mla_handle h, double* A, int64_t m, int64_t n, 
   return rc;
 }
 
+extern "C" int mla_release_host_cache(mla_handle h) {
+  if (!h) return MLA_E_INVALID;
+  cudaFree(h->a_dev); h->a_dev = nullptr; h->a_dev_bytes = 0;
+  cudaFree(h->ipiv_dev); h->ipiv_dev = nullptr; h->ipiv_dev_n = 0;
+  return MLA_OK;
+}
+
 extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_t ld_host,
                                  int32_t* ipiv_host, int b_outer, int b_inner, int variant, int sm_pf,
                                  int q_chunks, mla_lu_info* info_host) {
@@ -573,18 +587,22 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
 struct ApplyArgs {
   const double* P; int64_t ldp; int rows, w;
   double* T; int64_t ldt; int cols;
+  int skip_cols;            // leading columns of T that already carry the interchanges and their U rows
+  double* L; int64_t ldl; int left_cols;   // columns LEFT of the panel (interchanges only; nullable)
   PivPlan* plan; unsigned* ctrl; unsigned* flags; unsigned tag;
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
   extern __shared__ __align__(16) double smem[];
   const int nstrips = (a.cols + TRSM_CW - 1) / TRSM_CW;
+  const int nleft = (a.left_cols + LEFT_CW - 1) / LEFT_CW;
   const int rows_below = a.rows - a.w;
   const int tmc = (rows_below + GemmUpdateCfg::BM - 1) / GemmUpdateCfg::BM;
-  const int total = nstrips + nstrips * tmc;
+  const int first_gemm = nstrips + nleft;
+  const int total = first_gemm + nstrips * tmc;
   unsigned* next = a.ctrl + CW_QUEUE_NEXT;
   auto decode = [&](int t, int& strip, int& tm) {   // GEMM items, row-block-major (see gemm_tile_desc)
-    const int g = t - nstrips;
+    const int g = t - first_gemm;
     const int per_block = kRowBlockTiles * nstrips;
     const int rb = g / per_block;
     const int rows_here = imin(kRowBlockTiles, tmc - rb * kRowBlockTiles);
@@ -604,16 +622,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.ctrl + CW_ABORT, 0xBAD1u);
     return;
   }
-  int base = 0, ready_strip = -1;
+  int base = 0, ready_strip = -1, executed = 0;
   bool primed = false;
   int t = pop_item(next);
   while (t < total) {
+    ++executed;
     if (t < nstrips) {
-      const int c0 = t * TRSM_CW, cw = imin(TRSM_CW, a.cols - c0);
-      laswp_apply_cols(a.T + (int64_t)c0 * a.ldt, a.ldt, cw, a.plan->ref(), smem, kLaswpBufDoubles);
-      trsm_strip(a.P, a.w, a.ldp, a.T + (int64_t)c0 * a.ldt, cw, a.ldt, smem);
+      // PREP of strip t: interchanges + solve with the panel's unit-lower top block (lu.py:251-253, 280);
+      // columns below skip_cols are the leftover of an ET-cut panel and already hold both
+      const int c0 = t * TRSM_CW, c1 = imin(a.cols, c0 + TRSM_CW), lo = imax(c0, a.skip_cols);
+      if (lo < c1) {
+        laswp_apply_cols(a.T + (int64_t)lo * a.ldt, a.ldt, c1 - lo, a.plan->ref(), smem, kLaswpBufDoubles);
+        trsm_strip(a.P, a.w, a.ldp, a.T + (int64_t)lo * a.ldt, c1 - lo, a.ldt, smem);
+      }
       __syncthreads();
       if (threadIdx.x == 0) { __threadfence(); st_release(&a.flags[t], a.tag); }
+      primed = false;
+      t = pop_item(next);
+      continue;
+    }
+    if (t < first_gemm) {
+      // LEFT: the panel's interchanges for the owned columns to its left (lu.py:252, 329-332)
+      const int c0 = (t - nstrips) * LEFT_CW;
+      laswp_apply_cols(a.L + (int64_t)c0 * a.ldl, a.ldl, imin(LEFT_CW, a.left_cols - c0), a.plan->ref(), smem,
+                       kLaswpBufDoubles);
       primed = false;
       t = pop_item(next);
       continue;
@@ -630,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
     const int tn = pop_item(next);
     TileDesc nxt{};
     nxt.valid = false;
-    if (tn < total && tn >= nstrips && tile_kt<GemmUpdateCfg>(cur) >= GemmUpdateCfg::STAGES - 1) {
+    if (tn < total && tn >= first_gemm && tile_kt<GemmUpdateCfg>(cur) >= GemmUpdateCfg::STAGES - 1) {
       int s2, m2;
       decode(tn, s2, m2);
       if (s2 == ready_strip || flag_ready(&a.flags[s2], a.tag)) { ready_strip = s2; nxt = desc(s2, m2); }
@@ -639,7 +671,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
     primed = nxt.valid;
     t = tn;
   }
+  // Completion, once per CTA (all launches of the step count into the same word): the CTA whose report
+  // completes the queue publishes the step's tag -- the distributed driver's ru_done (lu.py:309-310),
+  // polled by the look-ahead panel running beside this kernel.
   bulk_wait_all();
+  __syncthreads();
+  if (threadIdx.x == 0 && executed > 0) {
+    __threadfence();
+    unsigned old = atom_add_release(a.ctrl + CW_QUEUE_DONE, (unsigned)executed);
+    if (old + (unsigned)executed == (unsigned)total) st_release(a.ctrl + CW_STEP_DONE, a.tag);
+  }
 }
 
 // prepare: interchange plan, empty queue, fresh flag tag.  launch: `ctas` CTAs (0 = update_sms / all) that
@@ -652,18 +693,22 @@ extern "C" int mla_apply_panel_prepare(mla_handle h, const int32_t* ipiv, int64_
   k_laswp_plan<<<1, 32, 0, s>>>(ipiv, (int)w, rows, 0, 0, 0, h->plan, h->ctrl);
   CK(h, cudaGetLastError());
   CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
+  CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_DONE, 0, sizeof(unsigned), s));
   ++h->apply_tag;
   return MLA_OK;
 }
 
 extern "C" int mla_apply_panel_launch(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
-                                      int64_t cols, int64_t ldt, int ctas, void* stream) {
-  if (!h || rows < w || w < 0 || cols < 0 || ctas < 0 || (rows > 0 && (ldp < rows || ldt < rows))) return MLA_E_INVALID;
-  if (w > kMaxPiv || cols > (int64_t)kMaxStrips * TRSM_CW) return MLA_E_INVALID;
-  if (w == 0 || cols == 0) return MLA_OK;
+                                      int64_t cols, int64_t ldt, int64_t skip_cols, double* L, int64_t left_cols,
+                                      int64_t ldl, int ctas, void* stream) {
+  if (!h || rows < w || w < 0 || cols < 0 || ctas < 0 || skip_cols < 0 || left_cols < 0) return MLA_E_INVALID;
+  if (rows > 0 && (ldp < rows || (cols > 0 && ldt < rows) || (left_cols > 0 && (ldl < rows || !L)))) return MLA_E_INVALID;
+  if (w > kMaxPiv || cols > (int64_t)kMaxStrips * TRSM_CW || left_cols >= (1ll << 31)) return MLA_E_INVALID;
+  if (w == 0 || (cols == 0 && left_cols == 0)) return MLA_OK;
   cudaStream_t s = (cudaStream_t)stream;
   CK(h, cudaFuncSetAttribute(k_apply_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
-  ApplyArgs a{P, ldp, (int)rows, (int)w, T, ldt, (int)cols, h->plan, h->ctrl, h->lu_state->rprep_done, h->apply_tag};
+  ApplyArgs a{P, ldp, (int)rows, (int)w, T, ldt, (int)cols, (int)(skip_cols < cols ? skip_cols : cols), L, ldl,
+              (int)left_cols, h->plan, h->ctrl, h->lu_state->rprep_done, h->apply_tag};
   void* args[] = {&a};
   int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
   if (h->update_sms > 0 && h->update_sms < grid) grid = h->update_sms;
@@ -679,7 +724,63 @@ extern "C" int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int6
   if (w == 0 || cols == 0) return MLA_OK;
   int rc = mla_apply_panel_prepare(h, ipiv, w, rows, stream);
   if (rc != MLA_OK) return rc;
-  return mla_apply_panel_launch(h, P, rows, w, ldp, T, cols, ldt, 0, stream);
+  return mla_apply_panel_launch(h, P, rows, w, ldp, T, cols, ldt, 0, nullptr, 0, 0, 0, stream);
+}
+
+extern "C" int mla_step_flag(mla_handle h, uint32_t** flag_dev, uint32_t* tag) {
+  if (!h) return MLA_E_INVALID;
+  if (flag_dev) *flag_dev = h->ctrl + CW_STEP_DONE;
+  if (tag) *tag = h->apply_tag;
+  return MLA_OK;
+}
+
+// ---- pack one factored panel for the broadcast (multi-GPU driver) ---------------------------------------
+// out: [4 x int32 header: factored width, singular, scheduled width, rows][w x int32 panel-local pivots, padded
+// to a multiple of 4][rows x w doubles, column-major, leading dimension rows].  The factored width and the
+// singular flag come from the info record the panel kernel of THIS handle left on the device, so the
+// whole chain panel -> pack -> broadcast is stream-ordered.
+__global__ void k_pack_panel(const double* __restrict__ P, int64_t ld, int64_t rows, int w, const int* __restrict__ ipiv,
+                             const mla_lu_info* info, int* out_i32, double* out_panel) {
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      out_i32[0] = info ? info->cols_factored : w;
+      out_i32[1] = info ? info->singular : 0;
+      out_i32[2] = w;
+      out_i32[3] = (int)rows;
+    }
+    for (int t = threadIdx.x; t < w; t += blockDim.x) out_i32[4 + t] = ipiv[t];
+  }
+  const int64_t half = rows >> 1;        // 16-byte moves when both sides are aligned
+  const bool vec = ((ld & 1) == 0) && ((rows & 1) == 0) && ((((uintptr_t)P | (uintptr_t)out_panel) & 15) == 0);
+  for (int c = blockIdx.y; c < w; c += gridDim.y) {
+    const double* src = P + (int64_t)c * ld;
+    double* dst = out_panel + (int64_t)c * rows;
+    if (vec) {
+      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < half; i += (int64_t)gridDim.x * blockDim.x)
+        reinterpret_cast<double2*>(dst)[i] = reinterpret_cast<const double2*>(src)[i];
+    } else {
+      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+    }
+  }
+}
+
+extern "C" int64_t mla_packed_panel_doubles(int64_t rows, int64_t w) {
+  if (rows < 0 || w < 0) return MLA_E_INVALID;
+  const int64_t ints = 4 + ((w + 3) & ~(int64_t)3);
+  return ints / 2 + rows * w;
+}
+
+extern "C" int mla_pack_panel(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ld, const int32_t* ipiv,
+                              int use_panel_info, double* out, void* stream) {
+  if (!h || !P || !ipiv || !out || rows < w || w < 1 || w > kMaxPiv || ld < rows) return MLA_E_INVALID;
+  const int64_t ints = 4 + ((w + 3) & ~(int64_t)3);
+  dim3 grid((unsigned)((rows / 2 + 255) / 256 > 16 ? 16 : ((rows / 2 + 255) / 256 < 1 ? 1 : (rows / 2 + 255) / 256)),
+            (unsigned)(w > 512 ? 512 : w));
+  k_pack_panel<<<grid, 256, 0, (cudaStream_t)stream>>>(P, ld, rows, (int)w, ipiv, use_panel_info ? h->info_dev : nullptr,
+                                                       reinterpret_cast<int*>(out), out + ints / 2);
+  CK(h, cudaGetLastError());
+  return MLA_OK;
 }
 
 // ---- fill_random -----------------------------------------------------------------------------------

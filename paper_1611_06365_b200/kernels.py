@@ -75,16 +75,8 @@ def laswp(a: torch.Tensor, piv, team=None, reverse: bool = False, pool=None, che
     if npiv == 0:
         return
     pool = pool or default_pool(a.device.index)
-    if npiv > MAX_PIVOT_BLOCK:
-        # validate the whole vector first (nothing may be touched on a bad index), then apply
-        # chunk by chunk on views that start at the chunk's first row
-        if bool(((ip < 0) | (ip >= rows)).any().item()):
-            raise IndexError("pivot index out of range for this view")
-        starts = list(range(0, npiv, MAX_PIVOT_BLOCK))
-        for t0 in (reversed(starts) if reverse else starts):
-            chunk = (ip[t0:t0 + MAX_PIVOT_BLOCK] - t0).contiguous()
-            laswp(a[t0:, :], chunk, reverse=reverse, pool=pool)
-        return
+    # pivot vectors longer than one device plan (MAX_PIVOT_BLOCK) are chunked inside the library, after
+    # the whole vector was range-checked on the device (nothing is touched on a bad index)
     fn = _capi.lib().mla_laswp if check else _capi.lib().mla_laswp_async   # async: no host sync
     _capi.check(fn(pool.handle, a.data_ptr(), rows, cols, ld, ip.data_ptr(), npiv,
                    int(bool(reverse)), _stream(a)), pool.handle, "laswp")
@@ -117,14 +109,59 @@ def apply_panel_prepare(piv, w: int, rows: int, device, pool=None, stream=None) 
                 "apply_panel_prepare")
 
 
-def apply_panel_launch(panel: torch.Tensor, w: int, target: torch.Tensor, ctas: int = 0, pool=None) -> None:
+def apply_panel_launch(panel: torch.Tensor, w: int, target: torch.Tensor | None, ctas: int = 0, pool=None,
+                       skip_cols: int = 0, left: torch.Tensor | None = None) -> None:
     """Second half of apply_panel on the current stream: `ctas` CTAs (0 = all) drain the prepared queue.
-    Launching it twice (two streams) makes the second launch join the first one's queue."""
+    Launching it twice (two streams) makes the second launch join the first one's queue.
+    `skip_cols`: leading columns of `target` that already carry the interchanges and their U rows (the
+    leftover of an ET-cut panel); `left`: the owned columns left of the panel (same first row), which
+    receive the interchanges only."""
     rows, pw, ldp = check_colmajor(panel, "panel")
-    trows, cols, ldt = check_colmajor(target, "target")
-    if trows != rows or w > pw or w > rows:
+    cols, ldt, tptr = 0, rows, 0
+    if target is not None and target.shape[1] > 0:
+        trows, cols, ldt = check_colmajor(target, "target")
+        tptr = target.data_ptr()
+        if trows != rows:
+            raise ValueError("apply_panel: panel/target shapes disagree")
+    if w > pw or w > rows:
         raise ValueError("apply_panel: panel/target shapes disagree")
-    pool = pool or default_pool(target.device.index)
-    _capi.check(_capi.lib().mla_apply_panel_launch(pool.handle, panel.data_ptr(), rows, w, ldp, target.data_ptr(),
-                                                   cols, ldt, int(ctas), _stream(target)), pool.handle,
-                "apply_panel_launch")
+    lcols, ldl, lptr = 0, rows, 0
+    if left is not None and left.shape[1] > 0:
+        lrows, lcols, ldl = check_colmajor(left, "left")
+        lptr = left.data_ptr()
+        if lrows != rows:
+            raise ValueError("apply_panel: left columns must start at the panel's first row")
+    pool = pool or default_pool(panel.device.index)
+    _capi.check(_capi.lib().mla_apply_panel_launch(pool.handle, panel.data_ptr(), rows, w, ldp, tptr, cols, ldt,
+                                                   int(skip_cols), lptr, lcols, ldl, int(ctas), _stream(panel)),
+                pool.handle, "apply_panel_launch")
+
+
+def step_flag(pool) -> tuple[int, int]:
+    """(device address of the pool's step flag, tag of the step prepared last): the flag equals the tag
+    once that update step's queue has been drained -- the ET flag for a panel running beside it."""
+    import ctypes
+    ptr, tag = ctypes.c_void_p(), ctypes.c_uint32()
+    _capi.check(_capi.lib().mla_step_flag(pool.handle, ctypes.byref(ptr), ctypes.byref(tag)), pool.handle, "step_flag")
+    return int(ptr.value), int(tag.value)
+
+
+PANEL_HDR_INT32 = 4     # factored width, singular, scheduled width, rows (mla_pack_panel)
+
+
+def packed_panel_doubles(rows: int, w: int) -> int:
+    return int(_capi.lib().mla_packed_panel_doubles(int(rows), int(w)))
+
+
+def pack_panel(panel: torch.Tensor, piv: torch.Tensor, out: torch.Tensor, pool=None, use_panel_info: bool = True) -> None:
+    """Factored panel (rows x w view of the matrix) + int32 pivots + header -> one contiguous broadcast
+    buffer (layout: include/mla_b200.h, mla_pack_panel).  Stream-ordered; the factored width comes from the
+    device-side record of the pool's last panel kernel."""
+    rows, w, ld = check_colmajor(panel, "panel")
+    if piv.dtype != torch.int32 or piv.shape[0] < w or out.dtype != torch.float64 or not out.is_contiguous() \
+            or out.numel() < packed_panel_doubles(rows, w):
+        raise ValueError("pack_panel: need int32 pivots and a contiguous float64 buffer of packed_panel_doubles()")
+    pool = pool or default_pool(panel.device.index)
+    _capi.check(_capi.lib().mla_pack_panel(pool.handle, panel.data_ptr(), rows, w, ld, piv.data_ptr(),
+                                           int(bool(use_panel_info)), out.data_ptr(), _stream(panel)), pool.handle,
+                "pack_panel")

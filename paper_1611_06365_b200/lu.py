@@ -44,6 +44,28 @@ def _check_tall(a: torch.Tensor) -> tuple[int, int, int]:
     return m, n, ld
 
 
+def _caller_ipiv(ipiv, n: int):
+    """Validate a caller-supplied pivot array like the reference's _shared_ipiv (lu.py:82-90): it must be
+    a 1-d int64 array of length >= n (numpy, or a torch tensor on the host or the device); the pivots are
+    written into its first n entries in place.  Returns a writer callback (or None)."""
+    if ipiv is None:
+        return None
+    if isinstance(ipiv, torch.Tensor):
+        if ipiv.dtype != torch.int64 or ipiv.dim() != 1 or ipiv.shape[0] < n:
+            raise ValueError("ipiv must be a 1-d int64 array of length >= n")
+        return lambda host, dev=None: ipiv[:host.shape[0]].copy_(
+            dev.to(torch.int64) if (dev is not None and ipiv.is_cuda) else torch.from_numpy(host))
+    arr = ipiv if isinstance(ipiv, np.ndarray) else np.asarray(ipiv)
+    if arr.dtype != np.int64 or arr.ndim != 1 or arr.shape[0] < n:
+        raise ValueError("ipiv must be a 1-d int64 array of length >= n")
+    # (anything that is not already an ndarray was converted to a private copy, exactly as
+    # np.asarray does in the reference: it validates, but the caller does not see the result)
+
+    def write(host, dev=None):
+        arr[:host.shape[0]] = host
+    return write
+
+
 class CountingStop:
     """Deterministic ET injection: behaves like a flag that is set from poll number `trip` on --
     the reference tests' CountingFlag fake (test_lu.py:149-156); trip=1 is a pre-set flag."""
@@ -62,6 +84,7 @@ def lu_blk_ll(a: torch.Tensor, b: int, ipiv=None, stop=None, team=None, cfg=None
     m, n, ld = _check_tall(a)
     if b < 1:
         raise ValueError("block size must be >= 1")
+    put = _caller_ipiv(ipiv, n)
     pool = pool or default_pool(a.device.index)
     if n == 0:
         return LuResult(PivotVector(np.empty(0, dtype=np.int64)), 0, False)
@@ -78,7 +101,10 @@ def lu_blk_ll(a: torch.Tensor, b: int, ipiv=None, stop=None, team=None, cfg=None
                                          flag_ptr, trip, int(team_sms or 0), ctypes.byref(info),
                                          _stream(a)), pool.handle, "lu_blk_ll")
     cols = int(info.cols_factored)
-    return LuResult(PivotVector(dev_piv[:cols].cpu().numpy(), device=dev_piv[:cols]), cols,
+    host_piv = dev_piv[:cols].cpu().numpy().astype(np.int64)
+    if put is not None:
+        put(host_piv, dev_piv[:cols])        # in place, like the reference (lu.py:160, 175)
+    return LuResult(PivotVector(host_piv, device=dev_piv[:cols]), cols,
                     bool(info.singular), int(info.et_events),
                     (cols,) if cols < n else ())
 
@@ -87,23 +113,28 @@ def lu_unb(a: torch.Tensor, ipiv=None, pool: SmPool | None = None) -> LuResult:
     """Unblocked pivoted LU (lu.py:97-103): the panel kernel with one block spanning the width
     (the device factors it in steps of at most 128 columns, which changes no pivot rule)."""
     m, n, _ = _check_tall(a)
-    return lu_blk_ll(a, max(n, 1), pool=pool)
+    return lu_blk_ll(a, max(n, 1), ipiv=ipiv, pool=pool)
 
 
 def lu_blk_ll_async(a: torch.Tensor, b: int, pool: SmPool, team_sms: int = 0,
-                    singular_accum: torch.Tensor | None = None) -> torch.Tensor:
+                    singular_accum: torch.Tensor | None = None, stop: tuple[int, int] | None = None,
+                    out: torch.Tensor | None = None) -> torch.Tensor:
     """Stream-ordered lu_blk_ll for drivers that never look at the result on the host: returns the
-    panel-local pivots as a device int32 tensor; `singular_accum` (device int32[1]) is OR-ed with the
-    singular flag.  No stop flag, no synchronisation."""
+    panel-local pivots as a device int32 tensor (`out` if given); `singular_accum` (device int32[1]) is
+    OR-ed with the singular flag; `stop` = (device address of a flag word, tag) is the ET flag of
+    lu.py:177-179 -- the panel is cut after a finished inner block once the word equals the tag.  The
+    factored width stays on the device (pool handle's info record; kernels.pack_panel reads it)."""
     m, n, ld = _check_tall(a)
     if b < 1:
         raise ValueError("block size must be >= 1")
-    dev_piv = torch.empty(n, dtype=torch.int32, device=a.device)
+    dev_piv = out if out is not None else torch.empty(n, dtype=torch.int32, device=a.device)
     if n == 0:
         return dev_piv
     acc = 0 if singular_accum is None else singular_accum.data_ptr()
+    flag_ptr, tag = (0, 0) if stop is None else (int(stop[0]), int(stop[1]))
     _capi.check(_capi.lib().mla_panel_ll_async(pool.handle, a.data_ptr(), m, n, ld, dev_piv.data_ptr(), int(b),
-                                               int(team_sms), acc, _stream(a)), pool.handle, "lu_blk_ll_async")
+                                               int(team_sms), acc, flag_ptr, tag, _stream(a)), pool.handle,
+                "lu_blk_ll_async")
     return dev_piv
 
 
@@ -114,6 +145,7 @@ def lu_blk_rl(a: torch.Tensor, b: int, ipiv=None, team=None, cfg=None, inner_b: 
     m, n, _ = _check_tall(a)
     if b < 1:
         raise ValueError("block size must be >= 1")
+    put = _caller_ipiv(ipiv, n)
     pool = pool or default_pool(a.device.index)
     ipiv_all = np.empty(n, dtype=np.int64)
     singular = False
@@ -127,6 +159,8 @@ def lu_blk_rl(a: torch.Tensor, b: int, ipiv=None, team=None, cfg=None, inner_b: 
         ipiv_all[j:j + w] = sub.ipiv.ipiv + j
         trsm_llu(a[j:j + w, j:j + w], a[j:j + w, j + w:n], pool=pool)
         gemm_malleable(a[j + w:m, j + w:n], a[j + w:m, j:j + w], a[j:j + w, j + w:n], 1.0, -1.0, pool=pool)
+    if put is not None:
+        put(ipiv_all)                          # global pivots, in place (lu.py:123-137)
     return LuResult(PivotVector(ipiv_all), n, singular)
 
 

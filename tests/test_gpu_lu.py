@@ -308,31 +308,68 @@ def test_full_config5_single_gpu(mla):
     assert r.cols_factored == 65536 and not r.singular
 
 
-def test_distributed_driver_single_rank_cuda(mla):
-    """The multi-GPU driver with its CUDA operator table, degenerate P=1 (one GPU in this run):
-    same pack/unpack/apply code path as under NCCL, minus the broadcast."""
+def _dist_check_vs_oracle(mla, dlu, a_host, ipiv, b_o, b_i, what):
+    """A DistLU run against the oracle REPLAYING its width schedule (panels clamped to column blocks)."""
+    from paper_1611_06365_b200.distributed import et_schedule_from_widths
+    n = a_host.shape[1]
+    ref = a_host.copy(order="F")
+    ro = oracle.lu_la(ref, b_o, b_i, et_sched=et_schedule_from_widths(dlu.widths, n, b_o, b_i, b_o), clamp=b_o)
+    assert tuple(ro.widths) == tuple(dlu.widths), f"{what}: width schedule not replayable"
+    assert sum(dlu.widths) == n and all(w % b_i == 0 for w in dlu.widths[:-1])
+    assert_parity(dlu.local_to_numpy(), ipiv, ref, ro.ipiv, what)
+    assert dlu.et_events == ro.et_events and bool(dlu.singular) == bool(ro.singular)
+
+
+@pytest.mark.parametrize("variant", ["lu", "lu_la", "lu_mb", "lu_et"])
+@pytest.mark.parametrize("n,b_o,b_i,dname", [(1536, 256, 32, "uniform"), (2000, 128, 16, "normal"), (300, 512, 64, "uniform")])
+def test_distributed_driver_single_rank_cuda(mla, variant, n, b_o, b_i, dname):
+    """The multi-GPU driver with its CUDA operator table, degenerate P=1 (one GPU in this run): same
+    pack/unpack/apply/look-ahead/ET code path as under NCCL, minus the broadcast.  Every variant of the
+    per-GPU step against the oracle; the non-ET variants never block the host."""
     from paper_1611_06365_b200.distributed import DistLU
     from paper_1611_06365_b200.workloads import LuConfig
-    n, b_o, b_i = 1536, 256, 32
-    cfg = LuConfig("t", n, "uniform", 4, b_o, b_i)
-    dlu = DistLU(n, b_o, b_i, cfg, "cuda", rank=0, world=1)
+    cfg = LuConfig("t", n, dname, 4, b_o, b_i)
+    dlu = DistLU(n, b_o, b_i, cfg, "cuda", variant=variant, rank=0, world=1)
     dlu.generate()
-    a_host = mla.make_matrix("uniform", n, 4)
+    a_host = mla.make_matrix(dname, n, 4)
     assert np.array_equal(dlu.local_to_numpy(), a_host)
     ipiv = dlu.factor()
-    ref = a_host.copy(order="F")
-    ro = oracle.lu_la(ref, b_o, b_i)
-    assert_parity(dlu.local_to_numpy(), ipiv, ref, ro.ipiv, "DistLU P=1")
+    _dist_check_vs_oracle(mla, dlu, a_host, ipiv, b_o, b_i, f"DistLU P=1 {variant} n={n}")
+    if variant != "lu_et":
+        assert dlu.et_events == 0 and dlu.host_waits == 0      # fully stream-ordered: zero host synchronisations
+    else:
+        assert dlu.host_waits == len(dlu.widths) - 1           # one mapped header read per look-ahead panel
+
+
+def test_distributed_driver_et_cuts_and_singular_flag(mla):
+    """ET on the device path fires (panel-bound sizes), the cut schedule is replayable, and a zero column is
+    reported through the broadcast header / device accumulator."""
+    from paper_1611_06365_b200.distributed import DistLU
+    n, b_o, b_i = 3072, 256, 32
+    a_host = mla.make_matrix("uniform", n, 0)
+    x = mla.from_numpy(a_host)
+    dlu = DistLU(n, b_o, b_i, None, x.device, variant="lu_et", rank=0, world=1, storage=x)
+    ipiv = dlu.factor()
+    assert dlu.et_events > 0
+    _dist_check_vs_oracle(mla, dlu, a_host, ipiv, b_o, b_i, "DistLU ET n=3072")
+    a_host = mla.make_matrix("uniform", 700, 1)
+    a_host[:, 300] = 0.0
+    for variant in ("lu_mb", "lu_et"):
+        x = mla.from_numpy(a_host)
+        dlu = DistLU(700, 128, 32, None, x.device, variant=variant, rank=0, world=1, storage=x)
+        ipiv = dlu.factor()
+        assert dlu.singular
+        _dist_check_vs_oracle(mla, dlu, a_host, ipiv, 128, 32, f"DistLU singular {variant}")
 
 
 @pytest.mark.parametrize("n,b_o,b_i", [(2000, 256, 32), (1111, 128, 16), (300, 512, 64)])
 def test_lu_streams_matches_the_oracle_and_lu_la(mla, n, b_o, b_i):
     """The multi-kernel single-GPU path (distributed driver with P = 1, in place on the caller's matrix):
-    pivots identical to the oracle's fixed-width schedule and to lu_la's lu_mb."""
+    pivots identical to the oracle's and to lu_la's."""
     a = gen(n, n, 9)
     d = mla.from_numpy(a)
-    from paper_1611_06365_b200.distributed import lu_streams
-    r = lu_streams(d, b_o, b_i)
+    from paper_1611_06365_b200.distributed import et_schedule_from_widths, lu_streams
+    r = lu_streams(d, b_o, b_i, variant="lu_mb")
     ref = a.copy(order="F")
     ro = oracle.lu_la(ref, b_o, b_i)
     assert_parity(mla.to_numpy(d), r.ipiv.ipiv, ref, ro.ipiv, f"lu_streams n={n}")
@@ -340,13 +377,20 @@ def test_lu_streams_matches_the_oracle_and_lu_la(mla, n, b_o, b_i):
     r2 = mla.lu_la(d2, mla.Policy("lu_mb", mla.BlockConfig(b_o, b_i)))
     assert np.array_equal(r.ipiv.ipiv, r2.ipiv.ipiv)
     assert tuple(r.widths) == tuple(r2.widths) and not r.singular
+    d3 = mla.from_numpy(a)
+    r3 = lu_streams(d3, b_o, b_i, variant="lu_et")
+    ref = a.copy(order="F")
+    ro = oracle.lu_la(ref, b_o, b_i, et_sched=et_schedule_from_widths(r3.widths, n, b_o, b_i, b_o), clamp=b_o)
+    assert tuple(ro.widths) == tuple(r3.widths) and r3.et_events == ro.et_events == len(r3.et_widths)
+    assert_parity(mla.to_numpy(d3), r3.ipiv.ipiv, ref, ro.ipiv, f"lu_streams lu_et n={n}")
 
 
-def test_distributed_driver_full_size_pivots_equal_lu_la(mla):
+@pytest.mark.parametrize("variant", ["lu_mb", "lu_et"])
+def test_distributed_driver_full_size_pivots_equal_lu_la(mla, variant):
     """The multi-GPU driver's CUDA path at a size with many row blocks and strips (P = 1, n = 16384,
-    b = 512/64): same pivot sequence as lu_la (whose pivots are pinned to the oracle's golden vectors at
-    this size by the full-config tests), twice in a row, and a small backward error.  The residual helper
-    permutes its first argument, hence the copies."""
+    b = 512/64), update and look-ahead panel CO-RESIDENT on the device (the mode that corrupted in round 1):
+    same pivot sequence as lu_la (whose pivots are pinned to the oracle's golden vectors at this size by the
+    full-config tests), twice in a row, and a small backward error."""
     from paper_1611_06365_b200.distributed import DistLU
     n, b_o, b_i = 16384, 512, 64
     a0 = mla.alloc_matrix(n, n)
@@ -356,13 +400,30 @@ def test_distributed_driver_full_size_pivots_equal_lu_la(mla):
     del x
     for _ in range(2):
         x = a0.clone()
-        dlu = DistLU(n, b_o, b_i, None, x.device, rank=0, world=1, storage=x)
+        dlu = DistLU(n, b_o, b_i, None, x.device, variant=variant, rank=0, world=1, storage=x)
         ipiv = dlu.factor()
         assert np.array_equal(ipiv, want)
         chk = a0.clone()
         berr = float(mla.residual_packed(chk, x, mla.PivotVector(ipiv))) / (n * EPS)
         assert berr <= BACKWARD_TOL
         del x, chk, dlu
+
+
+def test_distributed_driver_config5_single_rank(mla):
+    """Config 5 (n = 65536, b = 512/64, device-generated) through the multi-GPU driver's per-GPU step with
+    look-ahead + worker sharing + ET, P = 1: pivots identical to the LAPACK fixture, sampled rows / columns
+    within 1e-10, backward error <= 10 n eps.  (The >1-GPU layouts of the same driver are covered bitwise
+    under gloo in tests/test_distributed_cpu.py and with 2 ranks on this GPU below.)"""
+    from paper_1611_06365_b200.distributed import DistLU
+    cfg = mla.CONFIGS["config5"]
+    n = cfg.n
+    dlu = DistLU(n, cfg.b_outer, cfg.b_inner, cfg, "cuda", variant="lu_et", rank=0, world=1)
+    dlu.generate()
+    ipiv = dlu.factor()
+    _check_against_fixture(mla, "config5", dlu.a, ipiv, "DistLU config5 P=1")
+    berr = float(mla.residual_packed(dlu.a0, dlu.a, mla.PivotVector(ipiv))) / (n * EPS)   # destroys a0
+    assert berr <= BACKWARD_TOL
+    assert sum(dlu.widths) == n
 
 
 def test_device_trace_is_a_valid_reference_trace(mla, tmp_path):  # acceptance 4 (test_acceptance.py:192-218)

@@ -170,6 +170,54 @@ def test_laswp_golden_and_validation(mla, golden):  # test_kernels.py:329-332, 3
     mla.laswp(mla.alloc_matrix(5, 0), [1, 2])  # no columns: no-op
 
 
+def test_laswp_long_pivot_vectors_any_in_range_index(mla):
+    """More pivots than one device plan holds (1024): applied chunk by chunk inside the library.  The
+    reference's laswp accepts ANY index in [0, rows), also ipiv[t] < t (kernels.py:316-327) -- the chunks
+    must too -- and a bad index anywhere, including the last chunk, leaves the matrix untouched."""
+    rng = np.random.default_rng(99)
+    for rows, cols, npiv in [(3000, 40, 2500), (2100, 17, 2100), (1500, 9, 1025)]:
+        a = np.asfortranarray(rng.standard_normal((rows, cols)))
+        ipiv = rng.integers(0, rows, size=npiv).astype(np.int64)      # unconstrained: above and below t
+        d = mla.from_numpy(a)
+        mla.laswp(d, ipiv)
+        ref = a.copy(order="F")
+        oracle.laswp(ref, ipiv)
+        assert np.array_equal(mla.to_numpy(d), ref)
+        mla.laswp(d, ipiv, reverse=True)
+        assert np.array_equal(mla.to_numpy(d), a)
+        bad = ipiv.copy()
+        bad[-1] = rows                                                 # out of range in the LAST chunk
+        with pytest.raises(IndexError):
+            mla.laswp(d, bad)
+        assert np.array_equal(mla.to_numpy(d), a)                      # nothing was touched
+    # small vectors with indices above their position as well
+    a = np.asfortranarray(rng.standard_normal((50, 7)))
+    ipiv = np.array([49, 0, 1, 0, 48, 2], dtype=np.int64)
+    d = mla.from_numpy(a)
+    mla.laswp(d, ipiv)
+    ref = a.copy(order="F")
+    oracle.laswp(ref, ipiv)
+    assert np.array_equal(mla.to_numpy(d), ref)
+
+
+def test_caller_supplied_ipiv_is_written_in_place(mla):
+    """lu_unb / lu_blk_ll / lu_blk_rl honour a caller's pivot array like the reference (lu.py:82-90,
+    97-103, 123-137): 1-d int64 of length >= n, else ValueError; filled in place."""
+    a = gen(90, 60, 5)
+    for fn, kw in ((mla.lu_unb, {}), (lambda x, **k: mla.lu_blk_ll(x, 16, **k), {}),
+                   (lambda x, **k: mla.lu_blk_rl(x, 16, **k), {})):
+        mine = np.full(64, -7, dtype=np.int64)
+        r = fn(mla.from_numpy(a), ipiv=mine)
+        assert np.array_equal(mine[:60], r.ipiv.ipiv) and np.all(mine[60:] == -7)
+        dev = torch.full((60,), -7, dtype=torch.int64, device="cuda")
+        r2 = fn(mla.from_numpy(a), ipiv=dev)
+        assert np.array_equal(dev.cpu().numpy(), r2.ipiv.ipiv) and np.array_equal(r2.ipiv.ipiv, r.ipiv.ipiv)
+        for wrong in (np.zeros(59, dtype=np.int64), np.zeros(60, dtype=np.int32), np.zeros((60, 1), dtype=np.int64),
+                      torch.zeros(60, dtype=torch.int32)):
+            with pytest.raises(ValueError):
+                fn(mla.from_numpy(a), ipiv=wrong)
+
+
 # ---- panel (lu_unb / lu_blk_ll) -------------------------------------------------------------------
 
 def test_panel_kats(mla):  # test_lu.py:29-57

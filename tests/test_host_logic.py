@@ -136,3 +136,14 @@ def test_trace_rules_match_reference():  # reference trace.py:69-99 / test_trace
         check_trace([TraceEvent(0, "PF", "GEMM", 0, 10, 1), TraceEvent(0, "PF", "PANEL", 5, 50, 1)])
     with pytest.raises(ValueError):
         check_trace([TraceEvent(0, "PF", "NOPE", 0, 1, 1)])
+
+
+def test_packed_panel_layout_agrees_between_c_and_python():
+    """mla_pack_panel's buffer layout (header + int32 pivots + panel) as the C side sizes it must be what
+    distributed.py's views assume, for every scheduled width (ET makes widths vary per panel)."""
+    from paper_1611_06365_b200 import _capi
+    from paper_1611_06365_b200.distributed import DistLU
+    lib = _capi.lib()
+    for rows, w in [(65536, 512), (1216, 64), (300, 300), (97, 1), (1000, 24), (513, 130)]:
+        assert int(lib.mla_packed_panel_doubles(rows, w)) == DistLU._hdr_doubles(w) + rows * w
+        assert DistLU._hdr_doubles(w) * 2 >= 4 + w and (DistLU._hdr_doubles(w) * 8) % 16 == 0

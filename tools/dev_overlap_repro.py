@@ -1,11 +1,11 @@
-"""Reproducer of the round-1 corruption of the two-stream driver (panel kernel co-resident with the
-update kernel): P=1 DistLU(overlap_panel=True) on a device-generated uniform matrix; pivots compared with
-lu_la's, backward error from the device residual.
+"""Regression check for the round-1 corruption of the two-stream driver (panel kernel co-resident with the
+update kernel; root cause: a shared-memory race in the tile epilogue, fixed in round 2): P=1 DistLU in every
+variant on a device-generated uniform matrix; pivots compared with lu_la's, backward error from the device
+residual.
     python tools/dev_overlap_repro.py n b [reps]
 """
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["MLA_UNSAFE_OVERLAP"] = "1"
 import numpy as np, torch
 import paper_1611_06365_b200 as mla
 from paper_1611_06365_b200.distributed import DistLU
@@ -25,8 +25,8 @@ if n <= 40000:
     ref_piv = r.ipiv.ipiv.copy()
     del a
 bad = 0
-for overlap in (False, True):
-    dlu = DistLU(n, b, b // 8, cfg, "cuda", rank=0, world=1, overlap_panel=overlap)
+for overlap in ("lu", "lu_la", "lu_mb", "lu_et"):
+    dlu = DistLU(n, b, b // 8, cfg, "cuda", rank=0, world=1, variant=overlap)
     for rep in range(reps):
         dlu.a.copy_(a0); torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -38,6 +38,6 @@ for overlap in (False, True):
         same = None if ref_piv is None else bool(np.array_equal(piv, ref_piv))
         ok = berr <= 10 and same is not False
         bad += (not ok)
-        print(f"overlap={overlap} n={n} b={b} rep={rep}: {ms:.1f} ms  backward err {berr:.4g} n eps  pivots==lu_la {same}  {'OK' if ok else 'CORRUPT'}", flush=True)
+        print(f"variant={overlap} et_events={dlu.et_events} n={n} b={b} rep={rep}: {ms:.1f} ms  backward err {berr:.4g} n eps  pivots==lu_la {same}  {'OK' if ok else 'CORRUPT'}", flush=True)
     del dlu
 sys.exit(1 if bad else 0)
