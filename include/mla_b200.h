@@ -219,6 +219,27 @@ int mla_panel_profile(mla_handle h, uint64_t* out16, int reset);
  * [4] scheduled width << 32 | factored width.  Returns the number of rows copied. Synchronises. */
 int mla_getrf_trace(mla_handle h, uint64_t* out, int max_rows);
 
+/* Per-CTA device trace -- the GPU form of the reference's Tracer (trace.py:26-66: one private event buffer
+ * per worker, stamps from one clock).  After mla_set_trace(h, 1) every CTA of the persistent kernel appends
+ * one record per phase it runs (thread 0, globaltimer stamps taken where the phase actually starts and ends):
+ *   kind 1: drained the next panel's update queue (PF1/PF2 + RU helpers, lu.py:279-289)
+ *   kind 2: factored the look-ahead panel as a member of the panel team (PF3, lu.py:291)
+ *   kind 3: drained the remainder update queue as a member of the update team (RU1/RU2)
+ *   kind 4: the same queue, entered by a panel-team CTA AFTER its panel ended (worker sharing, pool.py:377-414;
+ *           the reference's MERGED team) -- stamped at the actual join
+ *   kind 5: panel factored by the whole grid (prologue, and every panel of variant "lu")
+ * mla_getrf_events copies max_per_cta records per CTA (unused records have kind 0) into out[cta][max_per_cta]
+ * and returns the number of CTAs (0 when tracing is off).  Synchronises the device. */
+typedef struct {
+  uint64_t t_start, t_end;   /* globaltimer ns */
+  int32_t iter;              /* outer iteration; 0 = prologue */
+  int32_t kind;
+  int32_t items;             /* queue items executed / panel columns factored */
+  int32_t team;              /* CTAs in the panel team of that iteration */
+} mla_trace_event;
+int mla_set_trace(mla_handle h, int enable);
+int mla_getrf_events(mla_handle h, mla_trace_event* out, int max_per_cta);
+
 /* Time accounting of one update-team CTA during the last mla_getrf_la call (ns): [0] in GEMM tiles,
  * [1] tile count, [2] in PREP items, [3] PREP count, [4] in LEFT items, [5] iteration barriers +
  * bookkeeping, [6] whole kernel. */

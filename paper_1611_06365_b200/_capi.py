@@ -7,7 +7,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmla_b200.so")
+LIB_PATH = os.environ.get("MLA_B200_LIB") or os.path.join(_HERE, "libmla_b200.so")   # override: A/B builds (tools/)
 
 OK, E_INVALID, E_CUDA, E_ABORT, E_INDEX, E_NOMEM = 0, -1, -2, -3, -4, -5
 VARIANT_CODES = {"lu": 0, "lu_la": 1, "lu_ws_static": 2, "lu_mb": 3, "lu_et": 4}
@@ -72,6 +72,10 @@ def lib() -> ctypes.CDLL:
     L.mla_pack_panel.restype = ctypes.c_int
     L.mla_packed_panel_doubles.argtypes = [_i64, _i64]
     L.mla_packed_panel_doubles.restype = _i64
+    L.mla_set_trace.argtypes = [_vp, ctypes.c_int]
+    L.mla_set_trace.restype = ctypes.c_int
+    L.mla_getrf_events.argtypes = [_vp, _vp, ctypes.c_int]
+    L.mla_getrf_events.restype = ctypes.c_int
     L.mla_release_host_cache.argtypes = [_vp]
     L.mla_release_host_cache.restype = ctypes.c_int
     L.mla_abort_word.argtypes = [_vp]
@@ -97,7 +101,7 @@ EXPORTS = ("mla_version", "mla_create", "mla_destroy", "mla_num_sms", "mla_last_
            "mla_getrf_la_sync", "mla_getrf_la_host", "mla_fill_random", "mla_panel_profile", "mla_getrf_trace", "mla_laswp_async", "mla_getrf_debug",
            "mla_apply_panel", "mla_set_panel_sms_max", "mla_panel_ll_async",
            "mla_set_update_sms", "mla_apply_panel_prepare", "mla_apply_panel_launch", "mla_abort_word",
-           "mla_step_flag", "mla_pack_panel", "mla_packed_panel_doubles", "mla_release_host_cache")
+           "mla_step_flag", "mla_set_trace", "mla_getrf_events", "mla_pack_panel", "mla_packed_panel_doubles", "mla_release_host_cache")
 
 
 class MlaError(RuntimeError):

@@ -74,6 +74,8 @@ def run_factorizations(args, writer) -> int:
     import paper_1611_06365_b200 as mla
     from paper_1611_06365_b200 import trace as mtrace
     pool = mla.default_pool()
+    if args.trace:
+        mtrace.enable(pool)
     ns = args.sweep_n if args.sweep_n else [args.n]
     bs = args.sweep_b if args.sweep_b else [args.b_outer]
     eps = float(np.finfo(np.float64).eps)
@@ -95,7 +97,7 @@ def run_factorizations(args, writer) -> int:
             torch.cuda.synchronize()
             wall = time.perf_counter() - t0
             if args.trace:
-                evs = mtrace.events_from_result(pool, result, args.algo, policy.t_pf)
+                evs = mtrace.events(pool)
                 mtrace.write_jsonl(evs, args.trace, append=not first)
                 first = False
             residual = None
@@ -107,6 +109,8 @@ def run_factorizations(args, writer) -> int:
                              f"{mla.flops_lu(n, n) / wall / 1e9:.4f}",
                              "" if residual is None else f"{residual:.17g}", result.et_events])
             sys.stdout.flush()
+    if args.trace:
+        mtrace.enable(pool, False)
     return worst
 
 

@@ -59,6 +59,7 @@ struct mla_handle_s {
   size_t ipiv_dev_n;
   double* resid_dev;
   unsigned apply_tag;    // per-call tag of the strip flags used by mla_apply_panel (never reused)
+  TraceEv* trace_dev;    // per-CTA event rings of the persistent kernel (nullptr: tracing off)
 };
 
 #define CK(h, call)                                   \
@@ -123,6 +124,7 @@ extern "C" int mla_destroy(mla_handle h) {
   cudaFree(h->resid_dev);
   cudaFree(h->a_dev);
   cudaFree(h->ipiv_dev);
+  cudaFree(h->trace_dev);
   if (h->s_main) cudaStreamDestroy(h->s_main);
   if (h->s_copy) cudaStreamDestroy(h->s_copy);
   if (h->ev_done) cudaEventDestroy(h->ev_done);
@@ -456,10 +458,9 @@ extern "C" int mla_set_update_sms(mla_handle h, int ctas) {
 }
 
 // ---- getrf (persistent kernel) ----------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 1) k_getrf(GetrfArgs a) {
-  extern __shared__ __align__(16) double smem[];
-  getrf_persistent(a, smem, kDynSmemDoubles);
-}
+static_assert(kDynSmemBytes == kGetrfSmemBytes, "both persistent kernels use the same shared-memory carve-up");
+int mla_launch_getrf(const GetrfArgs& a, int grid, int smem_bytes, cudaStream_t s);          // mla_getrf_prod.cu
+int mla_launch_getrf_traced(const GetrfArgs& a, int grid, int smem_bytes, cudaStream_t s);   // mla_getrf_traced.cu
 
 extern "C" int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
                             int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
@@ -474,16 +475,40 @@ extern "C" int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64
     if (info_dev) CK(h, cudaMemsetAsync(info_dev, 0, sizeof(mla_lu_info), s));
     return MLA_OK;
   }
-  CK(h, cudaFuncSetAttribute(k_getrf, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
   CK(h, cudaMemsetAsync(h->ctrl, 0, CW_COUNT * sizeof(unsigned), s));
   CK(h, cudaMemsetAsync(h->lu_state, 0, sizeof(LuState), s));
-  GetrfArgs a{A, (int)m, (int)n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks < 1 ? 1 : q_chunks,
-              h->sm_pf_max, h->next_progress, h->lu_state, h->plan, h->panel_ws, h->piv_local, h->ctrl, info_dev, widths, widths_cap};
-  h->next_progress = nullptr;
-  void* args[] = {&a};
   int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
-  CK(h, cudaLaunchCooperativeKernel((void*)k_getrf, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
+  if (h->trace_dev) CK(h, cudaMemsetAsync(h->trace_dev, 0, (size_t)grid * kTraceEvPerCta * sizeof(TraceEv), s));
+  GetrfArgs a{A, (int)m, (int)n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks < 1 ? 1 : q_chunks,
+              h->sm_pf_max, h->next_progress, h->lu_state, h->plan, h->panel_ws, h->piv_local, h->ctrl, info_dev, widths, widths_cap,
+              h->trace_dev};
+  h->next_progress = nullptr;
+  int e = h->trace_dev ? mla_launch_getrf_traced(a, grid, kDynSmemBytes, s) : mla_launch_getrf(a, grid, kDynSmemBytes, s);
+  if (e != 0) { h->last_cuda = e; return MLA_E_CUDA; }
   return MLA_OK;
+}
+
+// ---- per-CTA device trace of the persistent kernel (reference trace.py:26-66 Tracer) ---------------------
+extern "C" int mla_set_trace(mla_handle h, int enable) {
+  if (!h) return MLA_E_INVALID;
+  if (!enable) { cudaFree(h->trace_dev); h->trace_dev = nullptr; return MLA_OK; }
+  if (h->trace_dev) return MLA_OK;
+  int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
+  CK(h, cudaMalloc(&h->trace_dev, (size_t)grid * kTraceEvPerCta * sizeof(TraceEv)));
+  CK(h, cudaMemset(h->trace_dev, 0, (size_t)grid * kTraceEvPerCta * sizeof(TraceEv)));
+  return MLA_OK;
+}
+
+extern "C" int mla_getrf_events(mla_handle h, mla_trace_event* out, int max_per_cta) {
+  static_assert(sizeof(mla_trace_event) == sizeof(TraceEv), "trace record layout");
+  if (!h || !out || max_per_cta < 1) return MLA_E_INVALID;
+  if (!h->trace_dev) return 0;
+  CK(h, cudaDeviceSynchronize());
+  int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
+  int per = max_per_cta < kTraceEvPerCta ? max_per_cta : kTraceEvPerCta;
+  CK(h, cudaMemcpy2D(out, (size_t)max_per_cta * sizeof(TraceEv), h->trace_dev, (size_t)kTraceEvPerCta * sizeof(TraceEv),
+                     (size_t)per * sizeof(TraceEv), grid, cudaMemcpyDeviceToHost));
+  return grid;
 }
 
 extern "C" int mla_set_panel_sms_max(mla_handle h, int sm_pf_max) {

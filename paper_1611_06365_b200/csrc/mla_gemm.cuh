@@ -194,8 +194,11 @@ __device__ __forceinline__ void tile_prologue(const TileDesc& d, int base, doubl
 // previous tile's read + issue of the second half's operations [7] proxy fence of the second half
 __device__ unsigned long long g_tprof[8];
 #endif
+#ifndef MLA_TILE_ATTR
+#define MLA_TILE_ATTR
+#endif
 template <class Cfg>
-__device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, double* smem) {
+__device__ MLA_TILE_ATTR int tile_run(const TileDesc& d, const TileDesc& next, int base, double* smem) {
 #ifdef MLA_TILE_PROF
   const bool tp = blockIdx.x == 0 && threadIdx.x == 0;
   long long tp0 = clock64(), tpw = 0;
@@ -404,6 +407,11 @@ __device__ int tile_run(const TileDesc& d, const TileDesc& next, int base, doubl
 #endif
   return (base + KT) % STAGES;
 }
+
+// NOTE: the update's tile engine (tile_run<GemmUpdateCfg>) must stay INLINE in its kernels: compiled as an
+// out-of-line function, ptxas (12.9) allocates the bulk reduction's address operands in uniform registers
+// >= UR32 and UBLKRED then comes out as ADD.U64 instead of ADD.F64.RN (integer adds into C: garbage).
+// build.py scans the SASS of every build for exactly that.
 
 // One stand-alone C tile (no cross-tile prefetch).  A: mrem x K (lda), B: K x nrem (ldb),
 // Cin/Cout: mrem x nrem.  Collective over the CTA (256 threads); smem needs Cfg::SMEM_BYTES.

@@ -70,6 +70,20 @@ struct LuState {
 };
 constexpr int kTraceCap = 1024;
 
+// Per-CTA event record of the device trace (reference trace.py:16-23 TraceEvent, one private buffer per
+// worker, no locking on the hot path): every CTA's thread 0 appends one record per phase it ran.
+struct TraceEv {
+  unsigned long long t0, t1;     // globaltimer ns
+  int iter;                      // outer iteration (0 = prologue panel)
+  int kind;                      // TK_*
+  int items;                     // queue items executed (panel: columns factored)
+  int team;                      // CTAs in the panel team of that iteration
+};
+enum TraceKind { TK_PQ = 1, TK_PANEL = 2, TK_RQ = 3, TK_RQ_MERGED = 4, TK_PANEL_ALL = 5 };
+constexpr int kTraceEvPerCta = 4 * kTraceCap;
+constexpr int kGetrfSmemBytes = 218 * 1024;   // dynamic shared memory of the persistent kernels
+__host__ __device__ constexpr int mla_traced_smem_doubles() { return kGetrfSmemBytes / 8; }
+
 struct GetrfArgs {
   double* A; int m, n; int64_t ld;
   int* ipiv;                 // global pivots out (device int32[n])
@@ -83,6 +97,7 @@ struct GetrfArgs {
   unsigned* ctrl;            // CW_* words
   mla_lu_info* info;
   int* widths; int widths_cap;
+  TraceEv* tr;               // per-CTA event rings (kTraceEvPerCta records each) of the TRACED kernel, else unused
 };
 
 // item counts of one iteration, derived identically by every CTA from the descriptor
@@ -253,8 +268,11 @@ __device__ __forceinline__ QItem decode_item(const IterShape& s, int which, int 
 // (remainder + LEFT strips).  GEMM tiles run through the pipelined tile engine with a one-item
 // lookahead: while a tile finishes, the first k-slices of the next GEMM item (if its strip is already
 // prepared) are prefetched.  Returns the number of items executed, or -1 on abort.
-__device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* smem, int which,
-                                bool signal_ru_done) {
+#ifndef MLA_RQ_ATTR
+#define MLA_RQ_ATTR __forceinline__
+#endif
+__device__ MLA_RQ_ATTR int run_queue(const GetrfArgs& a, const IterShape& s, double* smem, int which,
+                                     bool signal_ru_done) {
   LuState* st = a.st;
   unsigned* next = which ? &st->rq_next : &st->pq_next;
   unsigned* done = which ? &st->rq_done : &st->pq_done;
@@ -306,7 +324,11 @@ __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* 
       const bool fut_issued = deep && have_tn && tn + 2 * (int)gridDim.x < total;
       if (fut_issued && threadIdx.x == 0)
         asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(fut) : "l"(next) : "memory");
+#ifdef MLA_NO_DBG
+      const bool dbgc = false;
+#else
       const bool dbgc = (blockIdx.x == gridDim.x - 1) && threadIdx.x == 0;
+#endif
       unsigned long long dt0 = dbgc ? globaltimer_ns() : 0ull;
       if (dbgc && primed && dbg_last_end) g_dbg[7] += dt0 - dbg_last_end;   // gap between chained tiles
       base = tile_run<GemmUpdateCfg>(cur, nxt, base, smem);
@@ -328,7 +350,11 @@ __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* 
       }
       continue;
     }
+#ifdef MLA_NO_DBG
+    const bool dbgc2 = false;
+#else
     const bool dbgc2 = (blockIdx.x == gridDim.x - 1) && threadIdx.x == 0;
+#endif
     unsigned long long dt1 = dbgc2 ? globaltimer_ns() : 0ull;
     if (it.kind == 1) {
       const int c0 = s.q1 + it.strip * TRSM_CW;
@@ -368,10 +394,10 @@ __device__ inline int run_queue(const GetrfArgs& a, const IterShape& s, double* 
   return executed;
 }
 
-__device__ inline bool run_pq(const GetrfArgs& a, const IterShape& s, double* smem) {
+__device__ __forceinline__ bool run_pq(const GetrfArgs& a, const IterShape& s, double* smem) {
   return run_queue(a, s, smem, 0, false) >= 0;
 }
-__device__ inline int run_rq(const GetrfArgs& a, const IterShape& s, double* smem, bool signal_ru_done) {
+__device__ __forceinline__ int run_rq(const GetrfArgs& a, const IterShape& s, double* smem, bool signal_ru_done) {
   return run_queue(a, s, smem, 1, signal_ru_done);
 }
 
@@ -379,7 +405,7 @@ __device__ inline int run_rq(const GetrfArgs& a, const IterShape& s, double* sme
 // Global pivots (lu.py:236,317: panel-local -> global) and the interchange plan of a factored panel
 // that starts at row/column q.  Collective over the CTA; kept out of line so that the persistent
 // kernel's tile loops do not depend on it.
-__device__ __noinline__ void publish_pivots(int* ipiv, const int* piv_local, int q, int k_new, int rows,
+static __device__ __noinline__ void publish_pivots(int* ipiv, const int* piv_local, int q, int k_new, int rows,
                                             PivPlan* plan, double* smem) {
   const int tid = threadIdx.x;
   for (int t = tid; t < k_new; t += kThreads) ipiv[q + t] = q + piv_local[t];
@@ -390,13 +416,33 @@ __device__ __noinline__ void publish_pivots(int* ipiv, const int* piv_local, int
   }
 }
 
-__device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int smem_doubles) {
+// Per-CTA control state of the persistent kernel.  It lives in SHARED memory, written by thread 0 only
+// (each write is separated from its readers by a __syncthreads): nothing of the outer loop's bookkeeping
+// is then live in registers across the tile loops of the queue drains, whose 128 accumulators + staging
+// addresses need the whole register file (with ~50 scalars of bookkeeping live across them ptxas either
+// spilled inside the k loop or re-derived the staging addresses there: 1830-2200 instead of ~1570
+// instructions per 32-deep k slice, 3-7 % of the whole factorization; round 2).
+struct KState {
+  unsigned all_target, pf_target;  // arrivals expected so far at the two team barriers
+  int ok;                          // 0 once an abort was observed
+  int sm_pf;                       // panel-team size of the current iteration
+  // bookkeeping carried from iteration to iteration (lu.py:314-326); only CTA 0's copy is used
+  int k_new, w_sched, q1_of_panel, b_target, singular, et_events, n_panels, ws_joins, q0, q1, it_next, prebuilt;
+  unsigned long long t_iter0, k_t0, b_t0;
+  // device trace (TRACE kernels): records written so far, start stamp of the running phase
+  int tr_n;
+  unsigned long long tr_t0;
+};
+
+// TRACE selects the instrumented twin (k_getrf_traced, its own translation unit): the production kernel
+// contains no tracing code at all.
+template <bool TRACE>
+__device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* smem, int smem_doubles) {
+  __shared__ KState ks;
+  __shared__ IterShape sh;         // this iteration's item counts, derived once per CTA (thread 0)
   LuState* st = a.st;
   const int G = gridDim.x, bid = blockIdx.x, tid = threadIdx.x;
-  unsigned* abort_word = a.ctrl;  // CW_ABORT == 0
-  Team all, pf;
-  all.init(bid, G, a.ctrl + 2 /*CW_BAR_ALL*/, abort_word);
-  pf.init(bid, G, a.ctrl + 3 /*CW_BAR_PF*/, abort_word);   // re-formed at the start of every iteration
+  unsigned* const abort_word = a.ctrl;  // CW_ABORT == 0
   const bool la = a.variant != MLA_VARIANT_LU && G >= 2;
   // Panel-team size.  Fixed at sm_pf (the reference's t_pf, restored every iteration, lu.py:270-273),
   // or -- with sm_pf_max > sm_pf -- malleable between iterations: doubled after an iteration in which
@@ -405,52 +451,82 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
   // team size; the factors only through the panel's device block width (slab fitting).
   const int sm_pf_lo = la ? imax(1, imin(a.sm_pf, G - 1)) : G;
   const int sm_pf_hi = la ? imax(sm_pf_lo, imin(a.sm_pf_max, G - 1)) : G;
-  int sm_pf = sm_pf_lo;
-  bool is_pf = la && bid < sm_pf;
-  unsigned long long t_iter0 = 0ull;
   const bool ws = la && (a.variant == MLA_VARIANT_LU_MB || a.variant == MLA_VARIANT_LU_ET ||
                          a.variant == MLA_VARIANT_LU_WS_STATIC);
   const bool et = la && a.variant == MLA_VARIANT_LU_ET;
   const int m = a.m, n = a.n;
-
-  // ---- prologue: first panel, the whole grid as one team (lu.py:224-241) --------------------------
-  const int w0 = imin(a.b_outer, n);
-  PanelResult pr = panel_ll(all, a.A, m, w0, a.ld, a.piv_local, a.b_inner, nullptr, 0u, 0, a.pws, smem, smem_doubles, true);
-  int k_new = pr.cols_factored;
-  int w_sched = w0;
-  int q1_of_panel = 0;       // where the just-factored panel starts
-  int b_target = a.b_outer;
-  int singular = pr.singular, et_events = 0, n_panels = 0, ws_joins = 0;
-  int q0 = 0, q1 = 0;
-
-  // The interchange plan is double-buffered by iteration parity: iteration `it` applies plan[it & 1]
-  // while the panel lead may already be writing plan[(it + 1) & 1].
-  int it_next = 1;
-  bool prebuilt = false;
   const bool dbgk = (bid == G - 1) && tid == 0;
+
+  if (tid == 0) {
+    ks.all_target = 0u; ks.pf_target = 0u; ks.ok = 1; ks.sm_pf = sm_pf_lo;
+    ks.k_new = 0; ks.w_sched = 0; ks.q1_of_panel = 0; ks.b_target = a.b_outer; ks.singular = 0; ks.et_events = 0;
+    ks.n_panels = 0; ks.ws_joins = 0; ks.q0 = 0; ks.q1 = 0; ks.it_next = 1; ks.prebuilt = 0;
+    ks.t_iter0 = 0ull; ks.tr_n = 0; ks.tr_t0 = 0ull;
+  }
   if (tid < 8) g_dbg[tid] = 0ull;
   __syncthreads();
-  const unsigned long long k_t0 = dbgk ? globaltimer_ns() : 0ull;
+
+  // A team exists in registers only for the duration of one collective (a barrier or a panel): it is
+  // rebuilt from the shared state and its counter written back, so no Team is live across a queue drain.
+  auto team_all = [&]() { Team t; t.init(bid, G, a.ctrl + 2 /*CW_BAR_ALL*/, abort_word, ks.all_target); t.ok = ks.ok != 0; return t; };
+  auto team_pf = [&]() { Team t; t.init(bid, ks.sm_pf, a.ctrl + 3 /*CW_BAR_PF*/, abort_word, ks.pf_target); t.ok = ks.ok != 0; return t; };
+  auto put_all = [&](const Team& t) { if (tid == 0) { ks.all_target = t.target; if (!t.ok) ks.ok = 0; } __syncthreads(); };
+  auto put_pf = [&](const Team& t) { if (tid == 0) { ks.pf_target = t.target; if (!t.ok) ks.ok = 0; } __syncthreads(); };
+  auto grid_barrier = [&]() -> bool { Team t = team_all(); t.barrier(); put_all(t); return ks.ok != 0; };
+  // device trace (TRACE only): thread 0 of every CTA appends (phase, t0, t1, iteration) records to its ring
+  auto tr_begin = [&]() {
+    if constexpr (TRACE) { if (tid == 0) ks.tr_t0 = globaltimer_ns(); }
+  };
+  auto tr_end = [&](int kind, int iter, int items, int team) {
+    if constexpr (TRACE) {
+      if (tid == 0 && ks.tr_n < kTraceEvPerCta) {
+        a.tr[(size_t)bid * kTraceEvPerCta + ks.tr_n] = TraceEv{ks.tr_t0, globaltimer_ns(), iter, kind, items, team};
+        ks.tr_n = ks.tr_n + 1;
+      }
+    }
+  };
+  // result of a panel this CTA took part in -> shared state (before anything long-running follows)
+  auto keep_panel_result = [&](const PanelResult& pr) {
+    if (tid == 0) { ks.k_new = pr.cols_factored; ks.singular |= pr.singular; }
+  };
+
+  // ---- prologue: first panel, the whole grid as one team (lu.py:224-241) --------------------------
+  {
+    const int w0 = imin(a.b_outer, n);
+    tr_begin();
+    Team t = team_all();
+    PanelResult pr = panel_ll(t, a.A, m, w0, a.ld, a.piv_local, a.b_inner, nullptr, 0u, 0, a.pws, smem, smem_doubles, true);
+    keep_panel_result(pr);
+    if (tid == 0) ks.w_sched = w0;
+    put_all(t);
+    tr_end(TK_PANEL_ALL, 0, pr.cols_factored, G);
+  }
+  if (dbgk) ks.k_t0 = globaltimer_ns();
+
+  // The interchange plan is double-buffered by iteration parity: iteration `it` applies plan[it & 1]
+  // while the panel lead may already be writing plan[(it + 1) & 1]  (ks.it_next counts the iterations).
   while (true) {
-    if (!all.ok) break;
+    if (!ks.ok) break;
     // ---- bookkeeping (lu.py:314-326) by CTA 0, between two grid barriers ----------------------------
-    unsigned long long b_t0 = dbgk ? globaltimer_ns() : 0ull;
-    all.barrier();
-    if (!all.ok) break;
+    if (dbgk) ks.b_t0 = globaltimer_ns();
+    if (!grid_barrier()) break;
     if (bid == 0) {
       // global pivots + interchange plan of the just-factored panel, unless the panel team's lead
       // already produced them right after its panel (look-ahead variants)
-      if (!prebuilt) {
-        publish_pivots(a.ipiv, a.piv_local, q1_of_panel, k_new, m - q1_of_panel, a.plan + (it_next & 1), smem);
+      if (!ks.prebuilt) {
+        publish_pivots(a.ipiv, a.piv_local, ks.q1_of_panel, ks.k_new, m - ks.q1_of_panel, a.plan + (ks.it_next & 1), smem);
       }
+      __syncthreads();
       if (tid == 0) {
+        const int k_new = ks.k_new, q1_of_panel = ks.q1_of_panel, w_sched = ks.w_sched;
+        int b_target = ks.b_target, n_panels = ks.n_panels, et_events = ks.et_events;
         if (a.widths && n_panels < a.widths_cap) a.widths[n_panels] = k_new;
         ++n_panels;
         if (k_new < w_sched) { ++et_events; b_target = imax(a.b_inner, k_new); }
         else if (q1_of_panel > 0) b_target = imin(a.b_outer, 2 * b_target);
-        int pend = q1_of_panel + w_sched;
-        q0 = q1_of_panel;
-        q1 = q1_of_panel + k_new;
+        const int pend = q1_of_panel + w_sched;
+        const int q0 = q1_of_panel, q1 = q1_of_panel + k_new;
+        ks.q0 = q0; ks.q1 = q1; ks.b_target = b_target; ks.n_panels = n_panels; ks.et_events = et_events;
         st->q0 = q0; st->q1 = q1; st->pend = pend;
         if (a.progress) {
           // every write to rows < q0 precedes the grid barrier above; later work touches rows >= q0 only
@@ -464,111 +540,136 @@ __device__ inline void getrf_persistent(const GetrfArgs& a, double* smem, int sm
         st->done = (q1 >= n) ? 1 : 0;
         st->pq_next = 0; st->pq_done = 0; st->rq_next = 0; st->rq_done = 0;
         if (la) {
-          int T = sm_pf;
+          int T = ks.sm_pf;
           if (sm_pf_hi > sm_pf_lo && q1_of_panel > 0) {
             const unsigned long long pe = *((volatile unsigned long long*)&st->t_panel_end);
             const unsigned long long rd = *((volatile unsigned long long*)&st->t_rq_done);
             if (rd == 0ull || pe > rd) T = imin(sm_pf_hi, 2 * T);
-            else if (3 * (pe - t_iter0) < (rd - t_iter0)) T = imax(sm_pf_lo, T / 2);
+            else if (3 * (pe - ks.t_iter0) < (rd - ks.t_iter0)) T = imax(sm_pf_lo, T / 2);
           }
           st->sm_pf_cur = T;
           if (T > st->sm_pf_peak) st->sm_pf_peak = T;
           st->t_rq_done = 0ull;
           a.ctrl[3 /*CW_BAR_PF*/] = 0u;   // nobody is inside a panel-team barrier here
         }
-        st->singular = singular; st->et_events = et_events; st->n_panels = n_panels; st->ws_joins = ws_joins;
+        st->singular = ks.singular; st->et_events = et_events; st->n_panels = n_panels; st->ws_joins = ks.ws_joins;
       }
     }
-    all.barrier();
-    if (dbgk) g_dbg[5] += globaltimer_ns() - b_t0;
-    if (!all.ok) break;
-    prebuilt = false;
-    ++it_next;
-    if (la) {
-      sm_pf = *((volatile const int*)&st->sm_pf_cur);
-      is_pf = bid < sm_pf;
-      pf.init(bid, sm_pf, a.ctrl + 3 /*CW_BAR_PF*/, abort_word);
-      if (bid == 0 && tid == 0) t_iter0 = globaltimer_ns();
+    if (!grid_barrier()) { if (dbgk) g_dbg[5] += globaltimer_ns() - ks.b_t0; break; }
+    if (dbgk) g_dbg[5] += globaltimer_ns() - ks.b_t0;
+    // ---- this iteration's descriptor -> shared memory (thread 0), then everybody reads it there ------
+    if (tid == 0) {
+      ks.prebuilt = 0;
+      ks.it_next = ks.it_next + 1;
+      if (la) {
+        ks.sm_pf = *((volatile const int*)&st->sm_pf_cur);
+        ks.pf_target = 0u;                                   // the panel team is re-formed every iteration
+        if (bid == 0) ks.t_iter0 = globaltimer_ns();
+      }
+      sh = iter_shape(st, m, n, G);
+      ks.q1_of_panel = sh.q1;
+      ks.w_sched = sh.w;
+      ks.b_target = *((volatile const int*)&st->b_target);
     }
-    IterShape s = iter_shape(st, m, n, G);
+    __syncthreads();
+    const bool is_pf = la && bid < ks.sm_pf;
     if (*((volatile const int*)&st->done)) {
       // ---- final_sync (lu.py:328-332): last panel's interchanges for the columns to its left ------
-      for (int l = bid; l < s.nleft; l += G) {
+      for (int l = bid; l < sh.nleft; l += G) {
         int c0 = l * LEFT_CW;
-        laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), (a.plan + (s.it & 1))->ref(), smem,
+        laswp_apply_cols(a.A + (int64_t)c0 * a.ld + sh.q0, a.ld, imin(LEFT_CW, sh.q0 - c0), (a.plan + (sh.it & 1))->ref(), smem,
                          kLaswpBufDoubles);
       }
       break;
     }
-    q1_of_panel = s.q1;
-    w_sched = s.w;
-    b_target = *((volatile const int*)&st->b_target);
-    const bool tr = s.it <= kTraceCap;
-    if (tr && bid == 0 && tid == 0) st->trace[s.it - 1][0] = globaltimer_ns();
+    const bool tr = sh.it <= kTraceCap;
+    if (tr && bid == 0 && tid == 0) st->trace[sh.it - 1][0] = globaltimer_ns();
 
     if (!la) {
       // ---- variant lu: update, then panel, one team (lu.py:259-269) --------------------------------
-      if (!run_pq(a, s, smem)) break;
-      if (run_rq(a, s, smem, false) < 0) break;
-      all.barrier();
-      if (!all.ok) break;
-      pr = panel_ll(all, a.A + (int64_t)s.q1 * a.ld + s.q1, m - s.q1, s.w, a.ld, a.piv_local, a.b_inner, nullptr,
-                    0u, 0, a.pws, smem, smem_doubles, true);
+      tr_begin();
+      const int e0 = run_queue(a, sh, smem, 0, false);
+      if (e0 < 0) break;
+      tr_end(TK_PQ, sh.it, e0, G);
+      tr_begin();
+      const int e1 = run_queue(a, sh, smem, 1, false);
+      if (e1 < 0) break;
+      tr_end(TK_RQ, sh.it, e1, G);
+      if (!grid_barrier()) break;
+      tr_begin();
+      Team t = team_all();
+      PanelResult pr = panel_ll(t, a.A + (int64_t)sh.q1 * a.ld + sh.q1, m - sh.q1, sh.w, a.ld, a.piv_local, a.b_inner, nullptr,
+                                0u, 0, a.pws, smem, smem_doubles, true);
+      keep_panel_result(pr);
+      put_all(t);
+      tr_end(TK_PANEL_ALL, sh.it, pr.cols_factored, G);
     } else {
       // ---- look-ahead: everybody drains PQ, then PF factors while RU updates (lu.py:270-312) --------
-      if (!run_pq(a, s, smem)) break;
+      tr_begin();
+      const int e0 = run_queue(a, sh, smem, 0, false);
+      if (e0 < 0) break;
+      tr_end(TK_PQ, sh.it, e0, ks.sm_pf);
       if (is_pf) {
         if (tid == 0) {
-          if (!spin_until_ge(&st->pq_done, (unsigned)s.pq_total, abort_word)) pf.ok = false;
+          if (!spin_until_ge(&st->pq_done, (unsigned)sh.pq_total, abort_word)) ks.ok = 0;
         }
         __syncthreads();
-        if (tr && bid == 0 && tid == 0) st->trace[s.it - 1][1] = globaltimer_ns();
-        pr = panel_ll(pf, a.A + (int64_t)s.q1 * a.ld + s.q1, m - s.q1, s.w, a.ld, a.piv_local, a.b_inner,
-                      et ? &st->ru_done : nullptr, (unsigned)s.it, 0, a.pws, smem, smem_doubles, true);
+        if (tr && bid == 0 && tid == 0) st->trace[sh.it - 1][1] = globaltimer_ns();
+        tr_begin();
+        Team t = team_pf();
+        PanelResult pr = panel_ll(t, a.A + (int64_t)sh.q1 * a.ld + sh.q1, m - sh.q1, sh.w, a.ld, a.piv_local, a.b_inner,
+                                  et ? &st->ru_done : nullptr, (unsigned)sh.it, 0, a.pws, smem, smem_doubles, true);
+        keep_panel_result(pr);
+        const bool pf_ok = t.ok;
+        put_pf(t);
+        tr_end(TK_PANEL, sh.it, pr.cols_factored, ks.sm_pf);
         if (bid == 0 && tid == 0) {
-          st_release(&st->pf_done, (unsigned)s.it);
+          st_release(&st->pf_done, (unsigned)sh.it);
           st->t_panel_end = globaltimer_ns();
           if (tr) {
-            st->trace[s.it - 1][2] = globaltimer_ns();
-            st->trace[s.it - 1][4] = ((unsigned long long)s.w << 32) | (unsigned)pr.cols_factored;
+            st->trace[sh.it - 1][2] = globaltimer_ns();
+            st->trace[sh.it - 1][4] = ((unsigned long long)sh.w << 32) | (unsigned)pr.cols_factored;
           }
         }
-        if (bid == 0 && pf.ok) {
+        if (bid == 0 && pf_ok) {
           // off the critical path of the update: the next iteration's pivots and plan
           __syncthreads();
-          publish_pivots(a.ipiv, a.piv_local, s.q1, pr.cols_factored, m - s.q1, a.plan + ((s.it + 1) & 1), smem);
+          publish_pivots(a.ipiv, a.piv_local, sh.q1, pr.cols_factored, m - sh.q1, a.plan + ((sh.it + 1) & 1), smem);
           __syncthreads();
-          prebuilt = true;
+          if (tid == 0) ks.prebuilt = 1;
         }
-        if (ws && pf.ok) {
+        if (!pf_ok) { if (tid == 0) atomicExch(abort_word, 0xDEAD4u); break; }
+        if (ws) {
           // worker sharing: the quiesced panel team joins the update queue (pool.py:377-414)
-          if (a.variant == MLA_VARIANT_LU_WS_STATIC && s.rq_total > 0) {
+          if (a.variant == MLA_VARIANT_LU_WS_STATIC && sh.rq_total > 0) {
             // join only at the next q-chunk boundary of the GEMM item range (lu.py:290-304)
             if (tid == 0) {
               int q = imax(1, a.q_chunks);
               unsigned head = ld_acquire(&st->rq_next);
-              int per = (s.rq_total + q - 1) / q;
+              int per = (sh.rq_total + q - 1) / q;
               int gpos = imax(0, (int)head);
               int next_chunk = ((gpos + per - 1) / per) * per;
-              unsigned wait_for = (unsigned)imin(next_chunk, s.rq_total);
+              unsigned wait_for = (unsigned)imin(next_chunk, sh.rq_total);
               spin_until_ge(&st->rq_next, wait_for, abort_word);
             }
             __syncthreads();
           }
-          int ex = run_rq(a, s, smem, et);
+          tr_begin();                                   // the actual join: after the team's last barrier
+          const int ex = run_queue(a, sh, smem, 1, et);
           if (ex < 0) break;
-          if (bid == 0 && ex > 0) ++ws_joins;
+          if (ex > 0) tr_end(TK_RQ_MERGED, sh.it, ex, ks.sm_pf);
+          if (bid == 0 && tid == 0 && ex > 0) ks.ws_joins = ks.ws_joins + 1;
         }
       } else {
-        if (run_rq(a, s, smem, et) < 0) break;
+        tr_begin();
+        const int ex = run_queue(a, sh, smem, 1, et);
+        if (ex < 0) break;
+        tr_end(TK_RQ, sh.it, ex, ks.sm_pf);
       }
     }
-    k_new = pr.cols_factored;
-    singular |= pr.singular;
-    if (is_pf && !pf.ok) { if (tid == 0) atomicExch(abort_word, 0xDEAD4u); }
   }
   if (dbgk) {
-    g_dbg[6] += globaltimer_ns() - k_t0;
+    g_dbg[6] += globaltimer_ns() - ks.k_t0;
     for (int i = 0; i < 8; ++i) st->dbg[i] = g_dbg[i];
   }
   if (bid == 0 && tid == 0 && a.info) {

@@ -427,21 +427,43 @@ def test_distributed_driver_config5_single_rank(mla):
 
 
 def test_device_trace_is_a_valid_reference_trace(mla, tmp_path):  # acceptance 4 (test_acceptance.py:192-218)
+    """Per-CTA device trace (every CTA records the phases it ran, MERGED stamped at the actual join):
+    structurally valid, round-trips through the reference's JSONL form, and shows worker sharing."""
     from paper_1611_06365_b200 import trace as mtrace
     pool = mla.default_pool()
     a = mla.alloc_matrix(12288, 12288)
     mla.fill_random(a, 0, 2.0, -1.0)
-    r = mla.lu_la(a, mla.Policy("lu_mb", mla.BlockConfig(256, 32), t_pf=48), pool)
-    evs = mtrace.events_from_result(pool, r, "lu_mb", 48)
+    mtrace.enable(pool)
+    try:
+        r = mla.lu_la(a, mla.Policy("lu_mb", mla.BlockConfig(256, 32), t_pf=48), pool)
+        evs = mtrace.events(pool)
+    finally:
+        mtrace.enable(pool, False)
     assert evs
-    mtrace.check_trace(evs)
-    path = str(tmp_path / "trace.jsonl")
+    mtrace.validate(evs)
+    assert {e.worker for e in evs} == set(range(pool.t))           # every CTA of the grid is a worker
+    iters = len(r.widths) - 1
+    panel = [e for e in evs if e.team == "PF" and e.task == "PANEL"]
+    assert len(panel) == 48 * iters                                  # one record per team member and iteration
+    path = str(tmp_path / "trace.jsonl.gz")
     mtrace.write_jsonl(evs, path)
     assert mtrace.load_jsonl(path) == evs
     merged = {e.iter_index for e in evs if e.team == "MERGED"}
     assert merged and r.ws_joins > 0                 # panel SMs joined the update in some iterations
-    idle = mtrace.pf_idle_fraction(evs)
-    assert all(idle[it] < 0.10 for it in merged)     # with merging the panel worker has (almost) no idle gap
+    assert {e.worker for e in evs if e.team == "MERGED"} <= set(range(48))
+    idle = mtrace.idle_fraction(evs, worker=0)
+    assert all(idle[it] < 0.10 for it in sorted(merged)[:4])   # with merging the panel lead has (almost) no idle gap
+    # without worker sharing no CTA ever records a MERGED phase, and tracing off records nothing
+    mtrace.enable(pool)
+    try:
+        mla.fill_random(a, 0, 2.0, -1.0)
+        mla.lu_la(a, mla.Policy("lu_la", mla.BlockConfig(256, 32), t_pf=48), pool)
+        evs2 = mtrace.events(pool)
+    finally:
+        mtrace.enable(pool, False)
+    mtrace.validate(evs2)
+    assert evs2 and not any(e.team == "MERGED" for e in evs2)
+    assert mtrace.events(pool) == []
 
 
 def test_bench_cli_csv(mla, capsys):  # reference test_bench.py: header, seed reproducibility, --check gate

@@ -2,6 +2,7 @@
 exports every symbol include/mla_b200.h declares (no compute calls without a GPU)."""
 import os
 import re
+import sys
 
 import numpy as np
 import pytest
@@ -123,19 +124,86 @@ def test_bench_cli_argument_rules():  # reference test_bench.py: exit code 2 on 
     assert args.sweep_b == [32, 64, 96]
 
 
-def test_trace_rules_match_reference():  # reference trace.py:69-99 / test_trace.py
-    from paper_1611_06365_b200.trace import TraceEvent, check_trace, iteration_spans, pf_idle_fraction
+def _synthetic_traces():
+    from paper_1611_06365_b200.trace import TraceEvent
     ok = [TraceEvent(0, "PF", "GEMM", 0, 10, 1), TraceEvent(0, "PF", "PANEL", 10, 50, 1),
-          TraceEvent(0, "MERGED", "GEMM", 50, 80, 1), TraceEvent(16, "RU", "GEMM", 0, 80, 1)]
-    check_trace(ok)
-    assert iteration_spans(ok) == {1: (0, 80)}
-    assert abs(pf_idle_fraction(ok)[1]) < 1e-12
-    with pytest.raises(ValueError):   # merged before the panel ended
-        check_trace([TraceEvent(0, "PF", "PANEL", 10, 50, 1), TraceEvent(1, "MERGED", "GEMM", 40, 80, 1)])
-    with pytest.raises(ValueError):   # overlap on one worker
-        check_trace([TraceEvent(0, "PF", "GEMM", 0, 10, 1), TraceEvent(0, "PF", "PANEL", 5, 50, 1)])
-    with pytest.raises(ValueError):
-        check_trace([TraceEvent(0, "PF", "NOPE", 0, 1, 1)])
+          TraceEvent(1, "PF", "PANEL", 11, 52, 1), TraceEvent(0, "MERGED", "GEMM", 51, 80, 1),
+          TraceEvent(16, "RU", "GEMM", 0, 80, 1), TraceEvent(0, "ALL", "PANEL", -20, -1, 0)]
+    bad = {
+        "merged before any panel ended": [TraceEvent(0, "PF", "PANEL", 10, 50, 1), TraceEvent(1, "MERGED", "GEMM", 40, 80, 1)],
+        "merged without a panel": [TraceEvent(1, "MERGED", "GEMM", 40, 80, 2)],
+        "overlap on one worker": [TraceEvent(0, "PF", "GEMM", 0, 10, 1), TraceEvent(0, "PF", "PANEL", 5, 50, 1)],
+        "unknown task": [TraceEvent(0, "PF", "NOPE", 0, 1, 1)],
+        "negative duration": [TraceEvent(0, "RU", "GEMM", 5, 1, 1)],
+    }
+    return ok, bad
+
+
+def test_trace_rules():  # the structural rules of reference trace.py:69-99 on this package's checker
+    from paper_1611_06365_b200.trace import check_trace, idle_fraction, iteration_spans, validate
+    ok, bad = _synthetic_traces()
+    validate(ok)
+    assert check_trace is validate
+    assert iteration_spans(ok)[1] == (0, 80)
+    assert abs(idle_fraction(ok, worker=16)[1]) < 1e-12
+    for why, evs in bad.items():
+        with pytest.raises(ValueError):
+            validate(evs)
+
+
+GPU_TRACE = os.path.join(ROOT, "tests", "golden", "gpu_trace_lu_mb.jsonl.gz")
+
+
+@pytest.mark.skipif(not os.path.exists(GPU_TRACE), reason="no committed GPU trace")
+def test_committed_gpu_trace_is_valid_and_merges():
+    """A per-CTA trace recorded on a B200 (tests/golden/make_gpu_trace.py, lu_mb): structurally valid, every
+    CTA of the grid contributed, panel-team CTAs joined the update (MERGED) after their panel, and with
+    merging the panel team's lead has almost no idle gap in the early iterations (acceptance 4,
+    test_acceptance.py:192-218)."""
+    from paper_1611_06365_b200 import trace as mtrace
+    evs = mtrace.load_jsonl(GPU_TRACE)
+    mtrace.validate(evs)
+    workers = {e.worker for e in evs}
+    assert len(workers) >= 100 and workers == set(range(len(workers)))
+    merged = [e for e in evs if e.team == "MERGED"]
+    assert merged and all(e.t_start >= min(p.t_end for p in evs if p.team == "PF" and p.task == "PANEL"
+                                           and p.iter_index == e.iter_index) for e in merged[:200])
+    idle = mtrace.idle_fraction(evs, worker=0)
+    early = [it for it in sorted({e.iter_index for e in merged}) if it >= 1][:4]
+    assert early and all(idle[it] < 0.10 for it in early)
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/pkg/src/mla"), reason="reference not present (GPU box)")
+def test_reference_checker_accepts_gpu_traces_and_agrees_on_violations():
+    """the UNMODIFIED reference's check_trace / iteration_spans / load_jsonl run on the GPU
+    trace file, and the reference's checker and this package's agree on every synthetic good / bad trace."""
+    import gzip
+    import importlib.util
+    import tempfile
+    spec = importlib.util.spec_from_file_location("ref_trace", "/root/reference/pkg/src/mla/trace.py")
+    ref = importlib.util.module_from_spec(spec)
+    sys.modules["ref_trace"] = ref
+    spec.loader.exec_module(ref)
+    from paper_1611_06365_b200 import trace as mtrace
+    ok, bad = _synthetic_traces()
+    as_ref = lambda evs: [ref.TraceEvent(e.worker, e.team, e.task, e.t_start, e.t_end, e.iter_index) for e in evs]
+    ref.check_trace(as_ref(ok))
+    assert ref.iteration_spans(as_ref(ok)) == mtrace.spans(ok)
+    for why, evs in bad.items():
+        with pytest.raises(ValueError):
+            ref.check_trace(as_ref(evs))
+        with pytest.raises(ValueError):
+            mtrace.validate(evs)
+    if os.path.exists(GPU_TRACE):
+        with tempfile.NamedTemporaryFile("wb", suffix=".jsonl", delete=False) as tmp:
+            tmp.write(gzip.open(GPU_TRACE, "rb").read())
+        try:
+            revs = ref.load_jsonl(tmp.name)                 # the reference's own reader
+            ref.check_trace(revs)                           # ... and its own checker, unmodified
+            assert ref.iteration_spans(revs) == mtrace.spans(mtrace.load_jsonl(GPU_TRACE))
+            assert any(e.team == "MERGED" for e in revs)
+        finally:
+            os.unlink(tmp.name)
 
 
 def test_packed_panel_layout_agrees_between_c_and_python():
