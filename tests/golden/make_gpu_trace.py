@@ -2,7 +2,7 @@
 checker (run on a B200: `python tests/golden/make_gpu_trace.py`; writes tests/golden/gpu_trace_lu_mb.jsonl.gz
 next to this file, or into gpurun_out/ when that directory exists so that the file travels back).
 
-lu_mb, n = 6144, b = 256/32, 48 panel CTAs: 23 outer iterations x 148 CTAs, ~10 k events."""
+lu_mb, n = 12288, b = 256/32, 48 panel CTAs: 47 outer iterations x 148 CTAs, ~20 k events."""
 import os
 import sys
 
@@ -14,7 +14,7 @@ import paper_1611_06365_b200 as mla  # noqa: E402
 from paper_1611_06365_b200 import trace as mtrace  # noqa: E402
 
 pool = mla.default_pool()
-n = 6144
+n = 12288
 a = mla.alloc_matrix(n, n)
 mla.fill_random(a, 0, 2.0, -1.0)
 mla.lu_la(a, mla.Policy("lu_mb", mla.BlockConfig(256, 32), t_pf=48), pool)       # warm-up, untraced
