@@ -35,12 +35,12 @@ sys.path.insert(0, ROOT)
 from paper_1611_06365_b200.workloads import CONFIGS, flops_lu, make_matrix  # noqa: E402
 
 # DRAM bytes of ONE k_getrf launch on the default workload (n=32768, b=512/64, lu_et, sm_pf 32), from
-# `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` (profiles/r01_getrf_n32768_traffic.csv):
-# 493.3 GB read + 229.8 GB written; the algorithmic minimum (the trailing matrix read and written once
+# `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` (profiles/r02_getrf_n32768_traffic.csv):
+# 492.0 GB read + 230.0 GB written; the algorithmic minimum (the trailing matrix read and written once
 # per iteration) is 2 * 8 * n^3 / (3 b) = 367 GB at b = 512 (ET cuts make the effective b smaller).
-# At b=256/32 the same measurement gave 577.2 + 423.0 GB against a minimum of 733 GB.
-DEFAULT_WORKLOAD_DRAM_BYTES = 493252247808 + 229810838016
-DEFAULT_WORKLOAD_DRAM_SOURCE = ("profiles/r01_getrf_n32768_traffic.csv (ncu dram__bytes_read.sum + dram__bytes_write.sum of "
+# It cannot be measured by the run that prints it (ncu replays the launch), hence the constant + its source.
+DEFAULT_WORKLOAD_DRAM_BYTES = 492022877952 + 230014721280
+DEFAULT_WORKLOAD_DRAM_SOURCE = ("profiles/r02_getrf_n32768_traffic.csv (ncu dram__bytes_read.sum + dram__bytes_write.sum of "
                                 "the k_getrf launch of this same command, captured in a separate run under ncu)")
 
 FP64_TENSOR_PEAK_TFLOPS = 37.0   # measured on this pool's B200: tools/fp64_peak.cu (DMMA.8x8x4

@@ -18,7 +18,7 @@ for d in rows:
     be = d.get("backward_error_over_n_eps", "")
     out.append("| %s | %s | %s | %.3f | %.3f | %.3f | %s | %s | %s | %s | %s |" % (
         c["workload"], c.get("variant"), c.get("sm_pf"), d["ms_per_step"], d["value"] / 1e3, d["value"] / 1e3 / 37.0,
-        ("%.4f" % be) if be != "" else "", c.get("et_events", ""), c.get("panels", ""),
+        ("%.4f" % be) if be != "" else "", d.get("run", c).get("et_events", ""), d.get("run", c).get("panels", ""),
         ("%.1f" % d["e2e"]["value"]) if d.get("e2e") else "", ("%.3f" % d["cpu_baseline"]["value"]) if d.get("cpu_baseline") else ""))
 open(f"profiles/{R}_results_table.md", "w").write("\n".join(out) + "\n")
 print("\n".join(out))
