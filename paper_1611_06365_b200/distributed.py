@@ -195,7 +195,7 @@ class DistLU:
     VARIANTS = ("lu", "lu_la", "lu_mb", "lu_et")
 
     def __init__(self, n, b_outer, b_inner, cfg, device, variant="lu_et", pool=None, ops=None, group=None,
-                 rank=None, world=None, panel_sms=32, comm_sms=8, storage=None, et_sched=None):
+                 rank=None, world=None, panel_sms=32, comm_sms=8, storage=None, et_sched=None, comm_always=False):
         if variant not in self.VARIANTS:
             raise ValueError(f"unknown variant {variant!r}; expected one of {self.VARIANTS}")
         if b_inner < 1 or b_outer < b_inner:
@@ -210,6 +210,9 @@ class DistLU:
         self.cuda = self.device.type == "cuda"
         self.ops = ops or CudaOps(pool)
         self.et_sched = list(et_sched) if et_sched is not None else None
+        # comm_always: issue the broadcasts (and use the communication stream) even with a single rank -- a
+        # 1-rank NCCL communicator exercises the whole collective path (stream handoff, buffer events) on one GPU
+        self.comm_always = bool(comm_always) and dist.is_available() and dist.is_initialized()
         self.nloc = self.map.local_cols(self.rank)
         # `storage`: factor the caller's (n x nloc, column-major) tensor in place instead of an own buffer
         self.a = storage if storage is not None else self.ops.alloc(n, max(self.nloc, 1), self.device)[:, :self.nloc]
@@ -330,7 +333,7 @@ class DistLU:
 
     # ---- exchange -------------------------------------------------------------------------------------
     def _bcast(self, which, q, w):
-        if self.P == 1:
+        if self.P == 1 and not self.comm_always:
             return
         src = self.map.owner(q // self.b)
         if self.group is not None:
@@ -345,8 +348,9 @@ class DistLU:
             self._bcast(which, q, w)
             hdr = self._views(which, self.n - q, w)[0]
             return int(hdr[0]), bool(int(hdr[1]))
-        stream = self.comm_stream if self.P > 1 else after
-        if self.P > 1:
+        use_comm = self.P > 1 or self.comm_always
+        stream = self.comm_stream if use_comm else after
+        if use_comm:
             if after is not None:                         # owner: the stream that packed the buffer
                 self.comm_stream.wait_stream(after)
             if self._buf_free[which] is not None:
@@ -401,7 +405,7 @@ class DistLU:
             it += 1
             q0, q1, pend = sched.q0, sched.q1, sched.pend
             kk, rows = q1 - q0, n - q0
-            if self.cuda and self.P > 1:
+            if self.cuda and (self.P > 1 or self.comm_always):
                 main.wait_stream(self.comm_stream)        # panel `cur` has arrived
             hdr, piv, panel = self._views(cur, rows, w_cur)
             self._piv_dev[q0:q1] = piv[:kk] + q0

@@ -498,6 +498,25 @@ def test_distributed_driver_two_ranks_cuda_ops(mla):
     assert out.stdout.count("pivots_equal=True") == 3
 
 
+def test_distributed_driver_nccl_communicator_one_rank(mla):
+    """The driver under a real NCCL process group (one rank: the most one GPU allows): every panel broadcast
+    goes through torch.distributed/NCCL on the communication stream with the buffer-reuse events, look-ahead
+    + WS + ET on; tools/dev_dist_nccl1.py asserts pivots, width replay and the 1e-10 factor bound."""
+    import socket
+    import subprocess
+    import sys
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "1", "--master-addr",
+                          "127.0.0.1", "--master-port", str(port), os.path.join(root, "tools", "dev_dist_nccl1.py")],
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert out.stdout.count("pivots_equal=True") == 3
+
+
 def test_random_small_shapes_property(mla):
     """Property sweep in the spirit of the reference's hypothesis tests (test_lu.py:247-256,
     test_kernels.py:366-401): random small m >= n, block widths and variants; pivots identical to the
