@@ -77,7 +77,9 @@ int mla_gemm(mla_handle h, double* C, int64_t m, int64_t n, int64_t ldc, const d
              const double* B, int64_t ldb, int64_t k, double alpha, double beta,
              const uint32_t* join_flag, int donor_ctas, void* stream);
 
-/* trsm_llu(a11, b) -- kernels.py:264-293.  B (w x c) := trilu(L)^-1 B, unit diagonal never read. */
+/* trsm_llu(a11, b) -- kernels.py:264-293.  B (w x c) := trilu(L)^-1 B, unit diagonal never read.  For
+ * w <= 1024 the solve runs in 128-row steps through the FP64 tensor-core tile engine with explicitly inverted
+ * 128 x 128 diagonal blocks (computed by a first small launch); beyond that in 32-row substitution steps. */
 int mla_trsm_llu(mla_handle h, const double* L, int64_t w, int64_t ldl, double* B, int64_t c,
                  int64_t ldb, void* stream);
 
@@ -162,8 +164,9 @@ int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_
 int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
                     int64_t cols, int64_t ldt, const int32_t* ipiv, void* stream);
 
-/* The two halves of mla_apply_panel.  prepare: interchange plan of the w pivots, empty work queue, fresh
- * step tag.  launch: `ctas` CTAs (0 = mla_set_update_sms / all) draining the prepared queue; a second
+/* The two halves of mla_apply_panel.  prepare: interchange plan of the w pivots, inverses of the 128 x 128
+ * diagonal blocks of the panel's unit-lower top block (the solves run in 128-row steps), empty work queue,
+ * fresh step tag.  launch: `ctas` CTAs (0 = mla_set_update_sms / all) draining the prepared queue; a second
  * launch of the same step on another stream JOINS that queue (worker sharing across kernels: the SMs that
  * factored the next panel help with the update once the panel is done, pool.py:377-414).
  *   skip_cols: leading columns of T that already carry the interchanges and their U rows (leftover of an
@@ -172,7 +175,8 @@ int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int64_t w, int6
  *              nullable): they receive the interchanges only (lu.py:252, 329-332), as extra queue items.
  * The CTA that completes the step's last item publishes the step tag in the handle's step flag
  * (mla_step_flag) -- the ru_done of lu.py:309-310 for a panel kernel running beside the update. */
-int mla_apply_panel_prepare(mla_handle h, const int32_t* ipiv, int64_t w, int64_t rows, void* stream);
+int mla_apply_panel_prepare(mla_handle h, const double* P, int64_t ldp, const int32_t* ipiv, int64_t w, int64_t rows,
+                            void* stream);
 int mla_apply_panel_launch(mla_handle h, const double* P, int64_t rows, int64_t w, int64_t ldp, double* T,
                            int64_t cols, int64_t ldt, int64_t skip_cols, double* L, int64_t left_cols, int64_t ldl,
                            int ctas, void* stream);

@@ -61,7 +61,7 @@ def lib() -> ctypes.CDLL:
     L.mla_panel_ll_async.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, ctypes.c_int, ctypes.c_int, _vp, _vp,
                                      ctypes.c_uint32, _vp]
     L.mla_panel_ll_async.restype = ctypes.c_int
-    L.mla_apply_panel_prepare.argtypes = [_vp, _vp, _i64, _i64, _vp]
+    L.mla_apply_panel_prepare.argtypes = [_vp, _vp, _i64, _vp, _i64, _i64, _vp]
     L.mla_apply_panel_prepare.restype = ctypes.c_int
     L.mla_apply_panel_launch.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _i64,
                                          ctypes.c_int, _vp]

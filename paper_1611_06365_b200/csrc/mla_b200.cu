@@ -60,6 +60,7 @@ struct mla_handle_s {
   double* resid_dev;
   unsigned apply_tag;    // per-call tag of the strip flags used by mla_apply_panel (never reused)
   TraceEv* trace_dev;    // per-CTA event rings of the persistent kernel (nullptr: tracing off)
+  DiagInv* dinv;         // device: inverted 128 x 128 diagonal blocks of the current panel(s), two sets
 };
 
 #define CK(h, call)                                   \
@@ -95,7 +96,8 @@ extern "C" int mla_create(int device, mla_handle* out) {
             cudaMalloc(&h->info_dev, sizeof(mla_lu_info)) == cudaSuccess &&
             cudaMallocHost(&h->info_host, sizeof(mla_lu_info)) == cudaSuccess &&
             cudaMalloc(&h->widths_dev, kWidthsCap * sizeof(int32_t)) == cudaSuccess &&
-            cudaMalloc(&h->resid_dev, 4 * sizeof(double)) == cudaSuccess;
+            cudaMalloc(&h->resid_dev, 4 * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&h->dinv, 2 * sizeof(DiagInv)) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&h->s_main, cudaStreamNonBlocking) == cudaSuccess &&
        cudaStreamCreateWithFlags(&h->s_copy, cudaStreamNonBlocking) == cudaSuccess &&
        cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming) == cudaSuccess &&
@@ -125,6 +127,7 @@ extern "C" int mla_destroy(mla_handle h) {
   cudaFree(h->a_dev);
   cudaFree(h->ipiv_dev);
   cudaFree(h->trace_dev);
+  cudaFree(h->dinv);
   if (h->s_main) cudaStreamDestroy(h->s_main);
   if (h->s_copy) cudaStreamDestroy(h->s_copy);
   if (h->ev_done) cudaEventDestroy(h->ev_done);
@@ -236,13 +239,31 @@ extern "C" int mla_gemm(mla_handle h, double* C, int64_t m, int64_t n, int64_t l
 
 
 // ---- trsm ------------------------------------------------------------------------------------------
+// Inverses of the 128 x 128 diagonal blocks of trilu(L) (one CTA per block) for the 128-row form of the solve.
 __global__ void __launch_bounds__(kThreads, 1)
-k_trsm(const double* L, int w, int64_t ldl, double* B, int64_t c, int64_t ldb) {
+k_diag_inv(const double* L, int w, int64_t ldl, DiagInv* out) {
+  extern __shared__ __align__(16) double smem[];
+  for (int blk = blockIdx.x; blk * TRSM_IB < w; blk += gridDim.x)
+    diag_block_inverse(L, blk * TRSM_IB, imin(TRSM_IB, w - blk * TRSM_IB), ldl, out->d[blk], smem);
+}
+
+static int launch_diag_inv(mla_handle h, const double* L, int64_t w, int64_t ldl, DiagInv* out, cudaStream_t s) {
+  const int smem_bytes = TRSM_SMEM_DOUBLES * 8;
+  CK(h, cudaFuncSetAttribute(k_diag_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  k_diag_inv<<<(unsigned)((w + TRSM_IB - 1) / TRSM_IB), kThreads, smem_bytes, s>>>(L, (int)w, ldl, out);
+  CK(h, cudaGetLastError());
+  return MLA_OK;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_trsm(const double* L, int w, int64_t ldl, double* B, int64_t c, int64_t ldb, const DiagInv* inv) {
   extern __shared__ __align__(16) double smem[];
   const int64_t strips = (c + TRSM_CW - 1) / TRSM_CW;
   for (int64_t s = blockIdx.x; s < strips; s += gridDim.x) {
     int64_t c0 = s * TRSM_CW;
-    trsm_strip(L, w, ldl, B + c0 * ldb, (int)(c - c0 < TRSM_CW ? c - c0 : TRSM_CW), ldb, smem);
+    const int cw = (int)(c - c0 < TRSM_CW ? c - c0 : TRSM_CW);
+    if (inv) trsm_strip_inv(L, w, ldl, B + c0 * ldb, cw, ldb, inv, smem);
+    else trsm_strip(L, w, ldl, B + c0 * ldb, cw, ldb, smem);
   }
 }
 
@@ -252,11 +273,17 @@ extern "C" int mla_trsm_llu(mla_handle h, const double* L, int64_t w, int64_t ld
   if (w <= 1 || c == 0) return MLA_OK;  // kernels.py:290: nothing to do
   if (ldl < w || ldb < w) return MLA_E_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  const int smem_bytes = TRSM_SMEM_DOUBLES * 8;
-  CK(h, cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  // 192 ... 1024 rows (full LU panels): 128-row steps with inverted diagonal blocks; else 32-row substitution
+  const bool blocked = w <= 1024 && trsm_use_inverse((int)w);
+  if (blocked) {
+    int rc = launch_diag_inv(h, L, w, ldl, h->dinv, s);
+    if (rc != MLA_OK) return rc;
+  }
+  const int smem_bytes = blocked ? GemmUpdateCfg::SMEM_BYTES : TRSM_SMEM_DOUBLES * 8;
+  CK(h, cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
   int64_t strips = (c + TRSM_CW - 1) / TRSM_CW;
   int grid = (int)(strips < h->num_sms ? strips : h->num_sms);
-  k_trsm<<<grid, kThreads, smem_bytes, s>>>(L, (int)w, ldl, B, c, ldb);
+  k_trsm<<<grid, kThreads, smem_bytes, s>>>(L, (int)w, ldl, B, c, ldb, blocked ? h->dinv : nullptr);
   CK(h, cudaGetLastError());
   return MLA_OK;
 }
@@ -481,7 +508,7 @@ extern "C" int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64
   if (h->trace_dev) CK(h, cudaMemsetAsync(h->trace_dev, 0, (size_t)grid * kTraceEvPerCta * sizeof(TraceEv), s));
   GetrfArgs a{A, (int)m, (int)n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks < 1 ? 1 : q_chunks,
               h->sm_pf_max, h->next_progress, h->lu_state, h->plan, h->panel_ws, h->piv_local, h->ctrl, info_dev, widths, widths_cap,
-              h->trace_dev};
+              h->trace_dev, h->dinv};
   h->next_progress = nullptr;
   int e = h->trace_dev ? mla_launch_getrf_traced(a, grid, kDynSmemBytes, s) : mla_launch_getrf(a, grid, kDynSmemBytes, s);
   if (e != 0) { h->last_cuda = e; return MLA_E_CUDA; }
@@ -615,6 +642,7 @@ struct ApplyArgs {
   int skip_cols;            // leading columns of T that already carry the interchanges and their U rows
   double* L; int64_t ldl; int left_cols;   // columns LEFT of the panel (interchanges only; nullable)
   PivPlan* plan; unsigned* ctrl; unsigned* flags; unsigned tag;
+  const DiagInv* inv;       // inverted diagonal blocks of the panel's unit-lower top block (mla_apply_panel_prepare)
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
@@ -658,7 +686,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
       const int c0 = t * TRSM_CW, c1 = imin(a.cols, c0 + TRSM_CW), lo = imax(c0, a.skip_cols);
       if (lo < c1) {
         laswp_apply_cols(a.T + (int64_t)lo * a.ldt, a.ldt, c1 - lo, a.plan->ref(), smem, kLaswpBufDoubles);
-        trsm_strip(a.P, a.w, a.ldp, a.T + (int64_t)lo * a.ldt, c1 - lo, a.ldt, smem);
+        if (trsm_use_inverse(a.w)) trsm_strip_inv(a.P, a.w, a.ldp, a.T + (int64_t)lo * a.ldt, c1 - lo, a.ldt, a.inv, smem);
+        else trsm_strip_ool(a.P, a.w, a.ldp, a.T + (int64_t)lo * a.ldt, c1 - lo, a.ldt, smem);
       }
       __syncthreads();
       if (threadIdx.x == 0) { __threadfence(); st_release(&a.flags[t], a.tag); }
@@ -711,10 +740,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
 // prepare: interchange plan, empty queue, fresh flag tag.  launch: `ctas` CTAs (0 = update_sms / all) that
 // drain the prepared queue; a second launch of the same step (other stream) joins the same queue -- the
 // distributed driver's worker sharing: the SMs that factored the next panel join the update when done.
-extern "C" int mla_apply_panel_prepare(mla_handle h, const int32_t* ipiv, int64_t w, int64_t rows, void* stream) {
-  if (!h || rows < w || w < 0 || w > kMaxPiv) return MLA_E_INVALID;
+extern "C" int mla_apply_panel_prepare(mla_handle h, const double* P, int64_t ldp, const int32_t* ipiv, int64_t w,
+                                       int64_t rows, void* stream) {
+  if (!h || !P || rows < w || w < 0 || w > kMaxPiv || ldp < rows) return MLA_E_INVALID;
   if (w == 0) return MLA_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (trsm_use_inverse((int)w)) { int rc = launch_diag_inv(h, P, w, ldp, h->dinv, s); if (rc != MLA_OK) return rc; }
   k_laswp_plan<<<1, 32, 0, s>>>(ipiv, (int)w, rows, 0, 0, 0, h->plan, h->ctrl);
   CK(h, cudaGetLastError());
   CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
@@ -733,7 +764,7 @@ extern "C" int mla_apply_panel_launch(mla_handle h, const double* P, int64_t row
   cudaStream_t s = (cudaStream_t)stream;
   CK(h, cudaFuncSetAttribute(k_apply_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
   ApplyArgs a{P, ldp, (int)rows, (int)w, T, ldt, (int)cols, (int)(skip_cols < cols ? skip_cols : cols), L, ldl,
-              (int)left_cols, h->plan, h->ctrl, h->lu_state->rprep_done, h->apply_tag};
+              (int)left_cols, h->plan, h->ctrl, h->lu_state->rprep_done, h->apply_tag, h->dinv};
   void* args[] = {&a};
   int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
   if (h->update_sms > 0 && h->update_sms < grid) grid = h->update_sms;
@@ -747,7 +778,7 @@ extern "C" int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int6
   if (!h || rows < w || w < 0 || cols < 0 || (rows > 0 && (ldp < rows || ldt < rows))) return MLA_E_INVALID;
   if (w > kMaxPiv || cols > (int64_t)kMaxStrips * TRSM_CW) return MLA_E_INVALID;
   if (w == 0 || cols == 0) return MLA_OK;
-  int rc = mla_apply_panel_prepare(h, ipiv, w, rows, stream);
+  int rc = mla_apply_panel_prepare(h, P, ldp, ipiv, w, rows, stream);
   if (rc != MLA_OK) return rc;
   return mla_apply_panel_launch(h, P, rows, w, ldp, T, cols, ldt, 0, nullptr, 0, 0, 0, stream);
 }

@@ -197,7 +197,9 @@ __device__ unsigned long long g_tprof[8];
 #ifndef MLA_TILE_ATTR
 #define MLA_TILE_ATTR
 #endif
-template <class Cfg>
+// RED = false compiles the tile without the bulk-reduction epilogue (plain read-modify-write instead): for
+// callers that live in out-of-line functions, where ptxas mis-encodes UBLKRED (see the note below).
+template <class Cfg, bool RED = true>
 __device__ MLA_TILE_ATTR int tile_run(const TileDesc& d, const TileDesc& next, int base, double* smem) {
 #ifdef MLA_TILE_PROF
   const bool tp = blockIdx.x == 0 && threadIdx.x == 0;
@@ -232,7 +234,7 @@ __device__ MLA_TILE_ATTR int tile_run(const TileDesc& d, const TileDesc& next, i
 #ifdef MLA_TILE_PROF
   long long tr0 = clock64();
 #endif
-  if constexpr (Cfg::FAST_OK) bulk_wait_read0();
+  if constexpr (RED && Cfg::FAST_OK) bulk_wait_read0();
 #ifdef MLA_TILE_PROF
   if (tp) g_tprof[6] += clock64() - tr0;
 #endif
@@ -302,7 +304,7 @@ __device__ MLA_TILE_ATTR int tile_run(const TileDesc& d, const TileDesc& next, i
   const bool vec = ((((uintptr_t)Cin | (uintptr_t)Cout) & 15) == 0) && ((ldcin & 1) == 0) && ((ldcout & 1) == 0);
   const bool full = vec && mrem == Cfg::BM && nrem == Cfg::BN;
   bool red_done = false;
-  if constexpr (Cfg::FAST_OK && Cfg::BM == 128 && Cfg::BN == 128 && Cfg::WJ == 4) {
+  if constexpr (RED && Cfg::FAST_OK && Cfg::BM == 128 && Cfg::BN == 128 && Cfg::WJ == 4) {
     if (full && alpha == 1.0 && beta == -1.0 && Cin == Cout && KT > 0 && __isGlobal(Cout)) {
       // C -= acc through the TMA engine: -acc is staged, half a tile (64 columns) at a time, in the ring
       // slot this tile consumed last, and added into C by one 1-KiB bulk reduction per column.
@@ -415,7 +417,7 @@ __device__ MLA_TILE_ATTR int tile_run(const TileDesc& d, const TileDesc& next, i
 
 // One stand-alone C tile (no cross-tile prefetch).  A: mrem x K (lda), B: K x nrem (ldb),
 // Cin/Cout: mrem x nrem.  Collective over the CTA (256 threads); smem needs Cfg::SMEM_BYTES.
-template <class Cfg>
+template <class Cfg, bool RED = true>
 __device__ void gemm_tile(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
                           int64_t ldb, int K, const double* Cin, int64_t ldcin, double* Cout,
                           int64_t ldcout, int mrem, int nrem, double alpha, double beta,
@@ -424,7 +426,7 @@ __device__ void gemm_tile(const double* __restrict__ A, int64_t lda, const doubl
   TileDesc none{};
   none.valid = false;
   tile_prologue<Cfg>(d, 0, smem);
-  tile_run<Cfg>(d, none, 0, smem);
+  tile_run<Cfg, RED>(d, none, 0, smem);
 }
 
 constexpr int kRowBlockTiles = 64;   // row tiles per L2 row block of the tile order

@@ -98,6 +98,7 @@ struct GetrfArgs {
   mla_lu_info* info;
   int* widths; int widths_cap;
   TraceEv* tr;               // per-CTA event rings (kTraceEvPerCta records each) of the TRACED kernel, else unused
+  DiagInv* dinv;             // two sets of inverted diagonal blocks: iteration `it` solves with set it & 1
 };
 
 // item counts of one iteration, derived identically by every CTA from the descriptor
@@ -154,7 +155,11 @@ __device__ inline void item_prep(const GetrfArgs& a, const IterShape& s, int c0,
   int lo = imax(c0, s.pend);
   if (lo < c0 + cw) {
     laswp_apply_cols(a.A + (int64_t)lo * a.ld + s.q0, a.ld, c0 + cw - lo, (a.plan + (s.it & 1))->ref(), smem, kLaswpBufDoubles);
-    trsm_strip(a.A + (int64_t)s.q0 * a.ld + s.q0, s.kk, a.ld, a.A + (int64_t)lo * a.ld + s.q0, c0 + cw - lo, a.ld, smem);
+    if (trsm_use_inverse(s.kk))
+      trsm_strip_inv(a.A + (int64_t)s.q0 * a.ld + s.q0, s.kk, a.ld, a.A + (int64_t)lo * a.ld + s.q0, c0 + cw - lo, a.ld,
+                     a.dinv + (s.it & 1), smem);
+    else
+      trsm_strip_ool(a.A + (int64_t)s.q0 * a.ld + s.q0, s.kk, a.ld, a.A + (int64_t)lo * a.ld + s.q0, c0 + cw - lo, a.ld, smem);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -489,6 +494,13 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
   auto keep_panel_result = [&](const PanelResult& pr) {
     if (tid == 0) { ks.k_new = pr.cols_factored; ks.singular |= pr.singular; }
   };
+  // the first members of the team that factored a panel invert its 128 x 128 diagonal blocks for the solves
+  // of the iteration that applies it (set (it_use) & 1); the panel's last team barrier made it visible
+  auto invert_diag_blocks = [&](const double* Lpanel, int k_new, int team_rank, int team_size, int it_use) {
+    if (!trsm_use_inverse(k_new)) return;
+    for (int blk = team_rank; blk * TRSM_IB < k_new; blk += team_size)
+      diag_block_inverse(Lpanel, blk * TRSM_IB, imin(TRSM_IB, k_new - blk * TRSM_IB), a.ld, (a.dinv + (it_use & 1))->d[blk], smem);
+  };
 
   // ---- prologue: first panel, the whole grid as one team (lu.py:224-241) --------------------------
   {
@@ -499,6 +511,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
     keep_panel_result(pr);
     if (tid == 0) ks.w_sched = w0;
     put_all(t);
+    invert_diag_blocks(a.A, pr.cols_factored, bid, G, 1);
     tr_end(TK_PANEL_ALL, 0, pr.cols_factored, G);
   }
   if (dbgk) ks.k_t0 = globaltimer_ns();
@@ -602,6 +615,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
                                 0u, 0, a.pws, smem, smem_doubles, true);
       keep_panel_result(pr);
       put_all(t);
+      invert_diag_blocks(a.A + (int64_t)sh.q1 * a.ld + sh.q1, pr.cols_factored, bid, G, sh.it + 1);
       tr_end(TK_PANEL_ALL, sh.it, pr.cols_factored, G);
     } else {
       // ---- look-ahead: everybody drains PQ, then PF factors while RU updates (lu.py:270-312) --------
@@ -622,6 +636,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
         keep_panel_result(pr);
         const bool pf_ok = t.ok;
         put_pf(t);
+        if (pf_ok) invert_diag_blocks(a.A + (int64_t)sh.q1 * a.ld + sh.q1, pr.cols_factored, bid, ks.sm_pf, sh.it + 1);
         tr_end(TK_PANEL, sh.it, pr.cols_factored, ks.sm_pf);
         if (bid == 0 && tid == 0) {
           st_release(&st->pf_done, (unsigned)sh.it);

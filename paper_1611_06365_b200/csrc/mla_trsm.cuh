@@ -70,4 +70,64 @@ __device__ inline void trsm_strip(const double* __restrict__ L, int w, int64_t l
   __syncthreads();
 }
 
+// ---- the solve in 128-row steps with explicitly inverted diagonal blocks --------------------------------------
+// For the update's PREP items (w = the panel width, up to 1024) the 32-row form above is latency-bound: 16
+// dependent steps of a 32 x 128 x r0 gemm + a 32-step substitution cost ~24 us each whatever their size.
+// Here a step is 128 rows and both of its parts are full tiles of the update's tile engine:
+//     T     = B[r0:r0+128] - L[r0:r0+128, 0:r0] @ X[0:r0]          (128 x 128 x r0)
+//     X[kb] = inv(trilu(L[kb,kb])) @ T                              (128 x 128 x 128)
+// 4 steps instead of 16 at w = 512.  The inverses D[kb] are computed once per panel (diag_block_inverse: the
+// substitution-based solve above applied to the identity) by whoever produced the panel.  trilu(L) of a
+// partial-pivoting panel has |l_ij| <= 1, its 128 x 128 blocks are well conditioned in practice; the
+// result differs from substitution in the last bits only (parity: tests/parity.py bound).
+constexpr int TRSM_IB = 128;
+constexpr int kMaxInvBlocks = 8;                 // panels of up to 1024 columns (kMaxPiv)
+// Below this many rows the 32-row substitution form is used: inverting the diagonal blocks costs ~60 us on the
+// path from a panel to the solves that use it, which narrow (ET-cut) panels do not earn back.
+constexpr int kInvMinRows = 192;
+__host__ __device__ constexpr bool trsm_use_inverse(int w) { return w >= kInvMinRows && w <= kMaxInvBlocks * TRSM_IB; }
+struct DiagInv { double d[kMaxInvBlocks][TRSM_IB * TRSM_IB]; };   // column-major blocks, leading dimension TRSM_IB
+
+// Collective over the CTA: out (ld TRSM_IB) = trilu(L[r0:r0+rb, r0:r0+rb])^-1, zero outside rb x rb.
+__device__ inline void diag_block_inverse(const double* __restrict__ L, int r0, int rb, int64_t ldl, double* out,
+                                          double* smem) {
+  __syncthreads();
+  for (int x = threadIdx.x; x < TRSM_IB * TRSM_IB; x += kThreads) {
+    const int c = x / TRSM_IB, i = x - c * TRSM_IB;
+    out[x] = (i == c && i < rb) ? 1.0 : 0.0;
+  }
+  __threadfence();
+  __syncthreads();
+  trsm_strip(L + (int64_t)r0 * ldl + r0, rb, ldl, out, rb, TRSM_IB, smem);
+  __threadfence();
+  __syncthreads();
+}
+
+// The substitution form as an out-of-line function, for the update's PREP items (a handful of call sites in
+// the persistent kernel: inlined, they change the register allocation of the tile loops around them).
+static __device__ __noinline__ void trsm_strip_ool(const double* __restrict__ L, int w, int64_t ldl, double* B, int cw,
+                                                   int64_t ldb, double* smem) {
+  trsm_strip(L, w, ldl, B, cw, ldb, smem);
+}
+
+// Collective over the CTA; smem needs GemmUpdateCfg::SMEM_BYTES.  Out of line on purpose (one copy of the
+// tile engine per kernel instead of one per call site); hence the tiles without the bulk reduction.
+static __device__ __noinline__ void trsm_strip_inv(const double* __restrict__ L, int w, int64_t ldl, double* B, int cw,
+                                            int64_t ldb, const DiagInv* inv, double* smem) {
+  int kb = 0;
+  for (int r0 = 0; r0 < w; r0 += TRSM_IB, ++kb) {
+    const int rb = imin(TRSM_IB, w - r0);
+    double* Bk = B + r0;
+    if (r0 > 0) {
+      gemm_tile<GemmUpdateCfg, false>(L + r0, ldl, B, ldb, r0, Bk, ldb, Bk, ldb, rb, cw, 1.0, -1.0, smem);
+      __threadfence();     // T (plain stores) must be in L2 before the next tile's cp.async reads it
+      __syncthreads();
+    }
+    // in place: every slice of T is staged (and consumed) before the epilogue's first store
+    gemm_tile<GemmUpdateCfg, false>(inv->d[kb], TRSM_IB, Bk, ldb, rb, Bk, ldb, Bk, ldb, rb, cw, 0.0, 1.0, smem);
+    __threadfence();
+    __syncthreads();
+  }
+}
+
 }  // namespace mla

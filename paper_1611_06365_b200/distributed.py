@@ -166,8 +166,8 @@ class CudaOps:
     def pack(self, panel, piv, out, side=False):
         self._k.pack_panel(panel, piv, out, pool=self.side_pool if side else self.pool)
 
-    def apply_prepare(self, piv, w, rows, device, side=False):
-        self._k.apply_panel_prepare(piv, w, rows, device, pool=self.side_pool if side else self.pool)
+    def apply_prepare(self, panel, piv, w, side=False):
+        self._k.apply_panel_prepare(panel, piv, w, pool=self.side_pool if side else self.pool)
 
     def apply_launch(self, panel, w, target, ctas=0, skip_cols=0, left=None, side=False):
         self._k.apply_panel_launch(panel, w, target, ctas, pool=self.side_pool if side else self.pool,
@@ -416,7 +416,7 @@ class DistLU:
                 # ---- final_sync (lu.py:329-332): last panel's interchanges for the columns to its left ----
                 if left_hi > 0:
                     if self.cuda:
-                        self.ops.apply_prepare(piv, kk, rows, self.device)
+                        self.ops.apply_prepare(panel, piv, kk)
                         self.ops.apply_launch(panel, kk, None, left=self.a[q0:, :left_hi])
                         self.launches_per_factor += 2
                     else:
@@ -447,7 +447,7 @@ class DistLU:
                 ready = None
                 if have_main:
                     self.ops.pool.set_update_sms(0)
-                    self.ops.apply_prepare(piv, kk, rows, self.device)
+                    self.ops.apply_prepare(panel, piv, kk)
                     ready = torch.cuda.Event()
                     ready.record(main)
                     self.ops.apply_launch(panel, kk, self.a[q0:, rest_lo:self.nloc],
@@ -458,7 +458,7 @@ class DistLU:
                         stop = self.ops.step_flag()
                 with torch.cuda.stream(side):
                     self.ops.side_pool.set_update_sms(self.panel_sms)
-                    self.ops.apply_prepare(piv, kk, rows, self.device, side=True)
+                    self.ops.apply_prepare(panel, piv, kk, side=True)
                     self.ops.apply_launch(panel, kk, self.a[q0:, lo1:lo1 + w], skip_cols=max(0, pend_lo - lo1), side=True)
                     self.ops.panel(nview, self.b_inner, self._piv_next, self._sing_dev, side=True,
                                    team_sms=self.panel_sms, stop=stop)
@@ -476,7 +476,7 @@ class DistLU:
                 # ---- no look-ahead overlap on this rank: update, then (owner) the panel on every SM --------
                 if self.nloc > lo1 or left_hi > 0:
                     self.ops.pool.set_update_sms(self.sms - self.comm_sms if self.P > 1 else 0)
-                    self.ops.apply_prepare(piv, kk, rows, self.device)
+                    self.ops.apply_prepare(panel, piv, kk)
                     self.ops.apply_launch(panel, kk, self.a[q0:, lo1:self.nloc], skip_cols=max(0, pend_lo - lo1),
                                           left=self.a[q0:, :left_hi])
                     self.launches_per_factor += 2

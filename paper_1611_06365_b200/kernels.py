@@ -98,15 +98,20 @@ def apply_panel(panel: torch.Tensor, w: int, target: torch.Tensor, piv, pool=Non
                                             ldt, ip.data_ptr(), _stream(target)), pool.handle, "apply_panel")
 
 
-def apply_panel_prepare(piv, w: int, rows: int, device, pool=None, stream=None) -> None:
-    """First half of apply_panel (plan, queue, tag); see apply_panel_launch."""
+def apply_panel_prepare(panel: torch.Tensor, piv, w: int, pool=None, stream=None) -> None:
+    """First half of apply_panel (interchange plan, inverted diagonal blocks of the panel's top block, queue,
+    tag); see apply_panel_launch."""
+    rows, pw, ldp = check_colmajor(panel, "panel")
+    if w > pw or w > rows:
+        raise ValueError("apply_panel: panel narrower than w")
+    device = panel.device
     pool = pool or default_pool(device.index)
     ip = _device_pivots(piv, device)
     if int(ip.shape[0]) < w:
         raise ValueError("apply_panel: need w pivots")
     st = torch.cuda.current_stream(device).cuda_stream if stream is None else stream
-    _capi.check(_capi.lib().mla_apply_panel_prepare(pool.handle, ip.data_ptr(), w, rows, st), pool.handle,
-                "apply_panel_prepare")
+    _capi.check(_capi.lib().mla_apply_panel_prepare(pool.handle, panel.data_ptr(), ldp, ip.data_ptr(), w, rows, st),
+                pool.handle, "apply_panel_prepare")
 
 
 def apply_panel_launch(panel: torch.Tensor, w: int, target: torch.Tensor | None, ctas: int = 0, pool=None,

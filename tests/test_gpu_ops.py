@@ -343,7 +343,7 @@ def test_apply_panel_second_launch_joins_the_queue(mla):
     piv_dev = torch.as_tensor(ipiv, dtype=torch.int32, device=got.device)
     main = torch.cuda.current_stream()
     side = torch.cuda.Stream()
-    apply_panel_prepare(piv_dev, w, rows, got.device)
+    apply_panel_prepare(dp, piv_dev, w)
     ready = torch.cuda.Event()
     ready.record(main)
     apply_panel_launch(dp, w, got, 100)
