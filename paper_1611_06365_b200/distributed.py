@@ -499,6 +499,9 @@ class DistLU:
         self.widths = tuple(sched.widths)
         self.et_events = sched.et_events
         if self.cuda:
+            # leave the shared handles as they were found: every SM for whoever launches an update next
+            self.ops.pool.set_update_sms(0)
+            self.ops.side_pool.set_update_sms(0)
             self.singular |= bool(int(self._sing_dev.item()))
             self.ipiv = self._piv_dev.cpu().numpy().astype(np.int64)   # the only bulk device->host copy
         else:
