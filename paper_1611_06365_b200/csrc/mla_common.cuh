@@ -139,6 +139,18 @@ __device__ __forceinline__ void grp_sync() {
   else asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / NT)), "n"(NT) : "memory");
 }
 
+// ---- race stress (tools/race_stress.sh) ---------------------------------------------------------------------
+// compute-sanitizer is closed on the GPU pool, so shared-memory races are hunted the crude way: a build with
+// -DMLA_RACE_STRESS delays SOME warps by a few microseconds at the points where a missing barrier would let a
+// fast warp overwrite what a slow one still reads; every deterministic result must stay bit-identical to the
+// normal build's.  (With the round-1 epilogue -- no barrier between the k loop and the staging stores -- this
+// build produces wrong factors at once: -DMLA_RACE_STRESS -DMLA_NO_EPILOGUE_BARRIER.)
+#ifdef MLA_RACE_STRESS
+#define MLA_STRESS(cond) do { if (cond) __nanosleep(4000); } while (0)
+#else
+#define MLA_STRESS(cond) do { } while (0)
+#endif
+
 __device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
 __device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
 

@@ -268,6 +268,7 @@ __device__ MLA_TILE_ATTR int tile_run(const TileDesc& d, const TileDesc& next, i
     double* const sdA = sdA0 + lslot * Cfg::STAGE;
     double* const sdB = sdB0 + lslot * Cfg::STAGE;
     if (!lfast) tile_issue<Cfg>(cur_tile ? d : next, lkt, lslot, smem);   // fringe / unaligned: whole slice at once
+    MLA_STRESS((warp & 1) == (kt & 1) && (kt % 5 == 4 || kt == KT - 1));   // skew the warps inside the k loop
     const double* sA = smem + ((base + kt) % STAGES) * Cfg::STAGE;
     const double* sB = sA + Cfg::A_STAGE;
     const double* pa = sA + q * Cfg::LDA_S + wi * Cfg::WTI + g;       // + k4*4*LDA_S + ni*8
@@ -312,7 +313,9 @@ __device__ MLA_TILE_ATTR int tile_run(const TileDesc& d, const TileDesc& next, i
       static_assert(64 * RED_LDS <= Cfg::STAGE, "staging fits one ring slot");
       // that slot is the one the k loop's LAST iteration read its fragments from: every warp must be
       // through with them before the first staging store lands there
+#ifndef MLA_NO_EPILOGUE_BARRIER
       grp_sync<Cfg::THREADS>();
+#endif
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         if ((wj >> 1) == half) {

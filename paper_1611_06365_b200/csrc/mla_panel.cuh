@@ -267,6 +267,7 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
       cand_warp_reduce(bv, br);
       const bool have = bv >= 0.0;
       const bool own_diag = (jc >= r0 && jc < r1);
+      MLA_STRESS((warp & 3) == (c & 3));            // skew the warps between the exchange and the deferred update
       if (warp != 0 && f2_c >= 0) {
         // F2 of the previous step on every row except warp 0's two
         const int64_t lcol = (int64_t)f2_c * lds;

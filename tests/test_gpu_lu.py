@@ -517,6 +517,26 @@ def test_distributed_driver_nccl_communicator_one_rank(mla):
     assert out.stdout.count("pivots_equal=True") == 3
 
 
+def test_results_do_not_depend_on_warp_timing(mla):
+    """Race hunt without compute-sanitizer (closed on the pool): tools/race_stress.sh runs the same deterministic
+    work (lu_mb at three shapes, k_gemm, k_apply_panel, k_panel) under the normal library and under a
+    -DMLA_RACE_STRESS build that delays some warps at the points where a missing barrier would bite; the
+    results must be bit-identical (and the build without round 2's epilogue barrier must differ).  Needs
+    build/lib_stress*.so newer than the sources (`tools/race_stress.sh build`); skipped otherwise."""
+    import glob
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libs = [os.path.join(root, "build", n) for n in ("lib_stress.so", "lib_stress_nofix.so")]
+    srcs = glob.glob(os.path.join(root, "paper_1611_06365_b200", "csrc", "*"))
+    if not all(os.path.exists(l) for l in libs) or min(os.path.getmtime(l) for l in libs) < max(os.path.getmtime(f) for f in srcs):
+        pytest.skip("stress libraries missing or older than the sources")
+    out = subprocess.run(["bash", os.path.join(root, "tools", "race_stress.sh")], capture_output=True, text=True,
+                         timeout=900, cwd=root)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "OK: no result depends on warp timing" in out.stdout
+    assert "the pre-fix epilogue is detected" in out.stdout
+
+
 def test_random_small_shapes_property(mla):
     """Property sweep in the spirit of the reference's hypothesis tests (test_lu.py:247-256,
     test_kernels.py:366-401): random small m >= n, block widths and variants; pivots identical to the
