@@ -162,6 +162,7 @@ __device__ inline void item_prep(const GetrfArgs& a, const IterShape& s, int c0,
       trsm_strip_ool(a.A + (int64_t)s.q0 * a.ld + s.q0, s.kk, a.ld, a.A + (int64_t)lo * a.ld + s.q0, c0 + cw - lo, a.ld, smem);
   }
   __syncthreads();
+  MLA_STRESS((blockIdx.x + s.it) % 3 == 1);        // ... and some publish their strip late
   if (threadIdx.x == 0) {
     __threadfence();
     st_release(flag, (unsigned)s.it);
@@ -288,6 +289,7 @@ __device__ MLA_RQ_ATTR int run_queue(const GetrfArgs& a, const IterShape& s, dou
   const int col_end = which ? a.n : (s.q1 + s.w);
   int executed = 0, base = 0;
   bool primed = false;
+  MLA_STRESS((blockIdx.x + s.it) % 5 == 0);        // some CTAs arrive late at the queue
   // Long queues (>= 16 tiles per CTA) pop one item further ahead with an atomic whose round trip
   // overlaps the running tile's main loop; short queues keep the shallow lookahead so the last
   // tiles of the iteration are not hoarded by one CTA.
@@ -629,6 +631,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
         }
         __syncthreads();
         if (tr && bid == 0 && tid == 0) st->trace[sh.it - 1][1] = globaltimer_ns();
+        MLA_STRESS((bid + sh.it) % 4 == 2);
         tr_begin();
         Team t = team_pf();
         PanelResult pr = panel_ll(t, a.A + (int64_t)sh.q1 * a.ld + sh.q1, m - sh.q1, sh.w, a.ld, a.piv_local, a.b_inner,
