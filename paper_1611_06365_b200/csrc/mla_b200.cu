@@ -677,7 +677,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
   }
   int base = 0, ready_strip = -1, executed = 0;
   bool primed = false;
+  __shared__ StripCache s_cache;     // strip flags this CTA has already seen set (one L2 trip per strip, not per tile)
+  s_cache.clear();
   int t = pop_item(next);
+  int tn = -1;                       // item popped ahead (-1: none)
+  auto advance = [&]() { if (tn >= 0) { t = tn; tn = -1; } else t = pop_item(next); };
   while (t < total) {
     ++executed;
     if (t < nstrips) {
@@ -692,7 +696,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
       __syncthreads();
       if (threadIdx.x == 0) { __threadfence(); st_release(&a.flags[t], a.tag); }
       primed = false;
-      t = pop_item(next);
+      advance();
       continue;
     }
     if (t < first_gemm) {
@@ -701,29 +705,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
       laswp_apply_cols(a.L + (int64_t)c0 * a.ldl, a.ldl, imin(LEFT_CW, a.left_cols - c0), a.plan->ref(), smem,
                        kLaswpBufDoubles);
       primed = false;
-      t = pop_item(next);
+      advance();
       continue;
     }
     int strip, tm;
     decode(t, strip, tm);
     TileDesc cur = desc(strip, tm);
     if (!primed) {
-      if (strip != ready_strip && !wait_flag_eq(&a.flags[strip], a.tag, a.ctrl + CW_ABORT)) return;
+      if (strip != ready_strip && !s_cache.has(strip)) {
+        if (!wait_flag_eq(&a.flags[strip], a.tag, a.ctrl + CW_ABORT)) return;
+        if (threadIdx.x == 0) s_cache.bits[strip >> 5] |= 1u << (strip & 31);   // read again only behind the next barrier
+      }
       ready_strip = strip;
       base = 0;
       tile_prologue<GemmUpdateCfg>(cur, base, smem);
     }
-    const int tn = pop_item(next);
+    if (tn < 0) tn = pop_item(next);
     TileDesc nxt{};
     nxt.valid = false;
     if (tn < total && tn >= first_gemm && tile_kt<GemmUpdateCfg>(cur) >= GemmUpdateCfg::STAGES - 1) {
       int s2, m2;
       decode(tn, s2, m2);
-      if (s2 == ready_strip || flag_ready(&a.flags[s2], a.tag)) { ready_strip = s2; nxt = desc(s2, m2); }
+      if (s2 == ready_strip || flag_ready_cached(s_cache, a.flags, s2, a.tag)) { ready_strip = s2; nxt = desc(s2, m2); }
     }
     base = tile_run<GemmUpdateCfg>(cur, nxt, base, smem);
     primed = nxt.valid;
     t = tn;
+    tn = -1;
   }
   // Completion, once per CTA (all launches of the step count into the same word): the CTA whose report
   // completes the queue publishes the step's tag -- the distributed driver's ru_done (lu.py:309-310),

@@ -218,6 +218,37 @@ __device__ inline bool flag_ready(const unsigned* flag, unsigned v) {
   return r;
 }
 
+// Per-CTA memory of the strip flags already seen set during the current queue drain.  A strip's flag is
+// written once per drain, so after the first acquire-load that finds it set, this CTA need not go back to L2
+// for it: with the row-block-major tile order consecutive tiles of a CTA lie in DIFFERENT strips, and the
+// L2 round trip of a flag test (~0.7 us) sat between every two chained tiles while the DMMA pipe idled.
+struct StripCache {
+  unsigned bits[kMaxStrips / 32];
+  __device__ __forceinline__ void clear() {      // collective over the CTA
+    __syncthreads();
+    for (int i = threadIdx.x; i < kMaxStrips / 32; i += blockDim.x) bits[i] = 0u;
+    __syncthreads();
+  }
+  __device__ __forceinline__ bool has(int strip) const { return (bits[strip >> 5] >> (strip & 31)) & 1u; }
+};
+
+// flag_ready with the cache in front: the fast path touches shared memory only.  All threads take the same
+// path (the bit is only ever written behind a barrier that every thread which read it as 0 takes part in).
+__device__ __forceinline__ bool flag_ready_cached(StripCache& sc, const unsigned* flags, int strip, unsigned v) {
+  if (sc.has(strip)) return true;
+  __shared__ int s_rdy2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int r = (ld_acquire(&flags[strip]) == v) ? 1 : 0;
+    s_rdy2 = r;
+    if (r) sc.bits[strip >> 5] |= 1u << (strip & 31);
+  }
+  __syncthreads();
+  const bool r = s_rdy2 != 0;
+  __syncthreads();
+  return r;
+}
+
 // Drain one of the two queues of the iteration.  which == 0: PQ (next panel's columns), 1: RQ
 // (remainder + LEFT strips).  GEMM tiles run through the pipelined tile engine with a one-item
 // lookahead: while a tile finishes, the first k-slices of the next GEMM item (if its strip is already
@@ -289,6 +320,8 @@ __device__ MLA_RQ_ATTR int run_queue(const GetrfArgs& a, const IterShape& s, dou
   const int col_end = which ? a.n : (s.q1 + s.w);
   int executed = 0, base = 0;
   bool primed = false;
+  __shared__ StripCache s_cache;
+  s_cache.clear();
   MLA_STRESS((blockIdx.x + s.it) % 5 == 0);        // some CTAs arrive late at the queue
   // Long queues (>= 16 tiles per CTA) pop one item further ahead with an atomic whose round trip
   // overlaps the running tile's main loop; short queues keep the shallow lookahead so the last
@@ -307,7 +340,10 @@ __device__ MLA_RQ_ATTR int run_queue(const GetrfArgs& a, const IterShape& s, dou
       const int c0 = col_base + strip * TRSM_CW;
       TileDesc cur = item_gemm_desc(a, s, it.tm, c0, imin(TRSM_CW, col_end - c0));
       if (!primed) {
-        if (strip != ready_strip && !wait_flag_eq(&flags[strip], (unsigned)s.it, a.ctrl)) return -1;
+        if (strip != ready_strip && !s_cache.has(strip)) {
+          if (!wait_flag_eq(&flags[strip], (unsigned)s.it, a.ctrl)) return -1;
+          if (threadIdx.x == 0) s_cache.bits[strip >> 5] |= 1u << (strip & 31);   // readers are behind the next barrier
+        }
         ready_strip = strip;
         base = 0;
         tile_prologue<GemmUpdateCfg>(cur, base, smem);
@@ -321,7 +357,7 @@ __device__ MLA_RQ_ATTR int run_queue(const GetrfArgs& a, const IterShape& s, dou
       // prologue was issued without knowing the successor
       if (have_tn && tn < total && tile_kt<GemmUpdateCfg>(cur) >= GemmUpdateCfg::STAGES - 1) {
         const QItem itn = decode_item(s, which, tn);
-        if (itn.kind == 3 && (itn.strip == ready_strip || flag_ready(&flags[itn.strip], (unsigned)s.it))) {
+        if (itn.kind == 3 && (itn.strip == ready_strip || flag_ready_cached(s_cache, flags, itn.strip, (unsigned)s.it))) {
           ready_strip = itn.strip;
           const int c2 = col_base + itn.strip * TRSM_CW;
           nxt = item_gemm_desc(a, s, itn.tm, c2, imin(TRSM_CW, col_end - c2));
