@@ -148,13 +148,27 @@ int mla_release_host_cache(mla_handle h);
  * factors on the device, downloads the packed factors and the pivots.  The download overlaps the
  * factorization: rows above the current panel are final (every later interchange, solve and update
  * touches lower rows only), the kernel reports that row through a mapped host word, and the finished
- * row blocks are copied out on a second stream while the kernel is still running.  Synchronous: the
+ * row blocks are copied out on a second stream while the kernel is still running.  The upload overlaps it as
+ * well (mla_set_host_phases below).  Synchronous: the
  * calling thread polls that word (50 us sleeps) and issues the copies.  The device copy of the matrix
  * (8 * m * n bytes, e.g. 8 GiB at n = 32768) and the pivot buffer stay cached in the handle for the next
  * call of the same or a smaller size, until mla_release_host_cache or mla_destroy. */
 int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_t ld_host,
                       int32_t* ipiv_host, int b_outer, int b_inner, int variant, int sm_pf,
                       int q_chunks, mla_lu_info* info_host);
+
+/* Windows of mla_getrf_la_host (the upload is overlapped too): the columns are uploaded in chunks and the
+ * factorization runs window by window behind the upload, left-looking between windows -- window [c0, c1) waits
+ * for its own chunk only, receives the interchanges / solves / rank-b updates of the columns [0, c0) factored so
+ * far, and is then factored by the persistent kernel restricted to it (look-ahead, WS and ET inside the window;
+ * lu_la's own iteration structure, lu.py:243-326, from column c0 on).  Every matrix entry sees the same operations
+ * in the same order as in an unwindowed run, so for the variants without ET the factors are bit-identical to
+ * mla_getrf_la's.  bounds/count: window ends in columns, ascending (rounded down to whole multiples of b_outer;
+ * the last window always ends at n); count == 0: one window (upload, then factor); count < 0 (default): windows
+ * end at n/32, n/16, n/8, n/4, 3n/8 for n >= 8192.  deep != 0: the catch-up of a window updates the rows below
+ * the factored block with ONE multiply of depth c0 instead of one rank-b update per block (fewer passes over the
+ * window; same result up to rounding, no longer bit-identical). */
+int mla_set_host_phases(mla_handle h, const int64_t* bounds, int count, int deep);
 
 /* One update step of the multi-GPU driver as a single persistent launch: apply the broadcast panel P
  * (rows x w: unit-lower L11 on top of L21, leading dimension ldp) with its w panel-local pivots to the

@@ -32,6 +32,7 @@ enum CtrlWord {
 
 constexpr int kDynSmemBytes = 218 * 1024;   // dynamic shared memory of the team kernels
 constexpr int kDynSmemDoubles = kDynSmemBytes / 8;
+constexpr int kMaxHostPhases = 16;
 
 struct mla_handle_s {
   int device;
@@ -61,6 +62,12 @@ struct mla_handle_s {
   unsigned apply_tag;    // per-call tag of the strip flags used by mla_apply_panel (never reused)
   TraceEv* trace_dev;    // per-CTA event rings of the persistent kernel (nullptr: tracing off)
   DiagInv* dinv;         // device: inverted 128 x 128 diagonal blocks of the current panel(s), two sets
+  // phased host entry point: upload stream, one event per uploaded column chunk, window boundaries
+  cudaStream_t s_up;
+  cudaEvent_t ev_up[kMaxHostPhases];
+  int phase_count;       // -1: default policy, 0: one phase (upload, then factor), > 0: explicit boundaries
+  int64_t phase_bounds[kMaxHostPhases];
+  int phase_deep;        // 1: catch-up updates as one deep multiply per window instead of one per panel
 };
 
 #define CK(h, call)                                   \
@@ -100,9 +107,13 @@ extern "C" int mla_create(int device, mla_handle* out) {
             cudaMalloc(&h->dinv, 2 * sizeof(DiagInv)) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&h->s_main, cudaStreamNonBlocking) == cudaSuccess &&
        cudaStreamCreateWithFlags(&h->s_copy, cudaStreamNonBlocking) == cudaSuccess &&
+       cudaStreamCreateWithFlags(&h->s_up, cudaStreamNonBlocking) == cudaSuccess &&
        cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming) == cudaSuccess &&
        cudaHostAlloc(&h->progress_host, 64, cudaHostAllocMapped) == cudaSuccess &&
        cudaHostGetDevicePointer(&h->progress_dev, h->progress_host, 0) == cudaSuccess;
+  for (int i = 0; ok && i < kMaxHostPhases; ++i)
+    ok = cudaEventCreateWithFlags(&h->ev_up[i], cudaEventDisableTiming) == cudaSuccess;
+  h->phase_count = -1;
   if (!ok) { mla_destroy(h); return MLA_E_NOMEM; }
   cudaMemset(h->plan, 0, 2 * sizeof(PivPlan));
   cudaMemset(h->panel_ws, 0, sizeof(PanelWs));
@@ -130,6 +141,8 @@ extern "C" int mla_destroy(mla_handle h) {
   cudaFree(h->dinv);
   if (h->s_main) cudaStreamDestroy(h->s_main);
   if (h->s_copy) cudaStreamDestroy(h->s_copy);
+  if (h->s_up) cudaStreamDestroy(h->s_up);
+  for (int i = 0; i < kMaxHostPhases; ++i) if (h->ev_up[i]) cudaEventDestroy(h->ev_up[i]);
   if (h->ev_done) cudaEventDestroy(h->ev_done);
   if (h->progress_host) cudaFreeHost(h->progress_host);
   delete h;
@@ -489,10 +502,22 @@ static_assert(kDynSmemBytes == kGetrfSmemBytes, "both persistent kernels use the
 int mla_launch_getrf(const GetrfArgs& a, int grid, int smem_bytes, cudaStream_t s);          // mla_getrf_prod.cu
 int mla_launch_getrf_traced(const GetrfArgs& a, int grid, int smem_bytes, cudaStream_t s);   // mla_getrf_traced.cu
 
+// One launch of the persistent kernel: columns [k0, n) of the m-row matrix (k0 > 0: a later window of the phased
+// host entry point -- columns [0, k0) are factored and applied, LuState carries on, a raised abort word stays).
+static int getrf_launch(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
+                        int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
+                        int32_t* widths, int widths_cap, int64_t k0, void* stream);
+
 extern "C" int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
                             int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
                             int32_t* widths, int widths_cap, void* stream) {
-  if (!h || m < n || n < 0 || (m > 0 && ld < m)) return MLA_E_INVALID;
+  return getrf_launch(h, A, m, n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks, info_dev, widths, widths_cap, 0, stream);
+}
+
+static int getrf_launch(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
+                        int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
+                        int32_t* widths, int widths_cap, int64_t k0, void* stream) {
+  if (!h || m < n || n < 0 || (m > 0 && ld < m) || k0 < 0 || (k0 > 0 && k0 >= n)) return MLA_E_INVALID;
   if (b_inner < 1 || b_outer < b_inner || b_outer > kMaxPiv) return MLA_E_INVALID;
   if (variant < MLA_VARIANT_LU || variant > MLA_VARIANT_LU_ET) return MLA_E_INVALID;
   if (n > (int64_t)kMaxStrips * TRSM_CW || m >= (1ll << 31)) return MLA_E_INVALID;
@@ -502,13 +527,17 @@ extern "C" int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64
     if (info_dev) CK(h, cudaMemsetAsync(info_dev, 0, sizeof(mla_lu_info), s));
     return MLA_OK;
   }
-  CK(h, cudaMemsetAsync(h->ctrl, 0, CW_COUNT * sizeof(unsigned), s));
-  CK(h, cudaMemsetAsync(h->lu_state, 0, sizeof(LuState), s));
   int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
-  if (h->trace_dev) CK(h, cudaMemsetAsync(h->trace_dev, 0, (size_t)grid * kTraceEvPerCta * sizeof(TraceEv), s));
+  if (k0 == 0) {
+    CK(h, cudaMemsetAsync(h->ctrl, 0, CW_COUNT * sizeof(unsigned), s));
+    CK(h, cudaMemsetAsync(h->lu_state, 0, sizeof(LuState), s));
+    if (h->trace_dev) CK(h, cudaMemsetAsync(h->trace_dev, 0, (size_t)grid * kTraceEvPerCta * sizeof(TraceEv), s));
+  } else {
+    CK(h, cudaMemsetAsync(h->ctrl + 1, 0, (CW_COUNT - 1) * sizeof(unsigned), s));   // CW_ABORT (word 0) stays
+  }
   GetrfArgs a{A, (int)m, (int)n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks < 1 ? 1 : q_chunks,
               h->sm_pf_max, h->next_progress, h->lu_state, h->plan, h->panel_ws, h->piv_local, h->ctrl, info_dev, widths, widths_cap,
-              h->trace_dev, h->dinv};
+              h->trace_dev, h->dinv, (int)k0};
   h->next_progress = nullptr;
   int e = h->trace_dev ? mla_launch_getrf_traced(a, grid, kDynSmemBytes, s) : mla_launch_getrf(a, grid, kDynSmemBytes, s);
   if (e != 0) { h->last_cuda = e; return MLA_E_CUDA; }
@@ -572,10 +601,45 @@ extern "C" int mla_release_host_cache(mla_handle h) {
   return MLA_OK;
 }
 
+static int catch_up(mla_handle h, double* A, int64_t m, int64_t ld, const int32_t* ipiv, int64_t k, int64_t c0,
+                    int64_t c1, int b_outer, bool deep, cudaStream_t s);
+
+extern "C" int mla_set_host_phases(mla_handle h, const int64_t* bounds, int count, int deep) {
+  if (!h || count > kMaxHostPhases - 1 || (count > 0 && !bounds)) return MLA_E_INVALID;
+  for (int i = 0; i < count; ++i)
+    if (bounds[i] <= (i ? bounds[i - 1] : 0)) return MLA_E_INVALID;
+  h->phase_count = count < 0 ? -1 : count;
+  for (int i = 0; i < count; ++i) h->phase_bounds[i] = bounds[i];
+  h->phase_deep = deep ? 1 : 0;
+  return MLA_OK;
+}
+
+// Window boundaries of the phased entry point: out[0] < out[1] < ... < out[np-1] == n.  Default policy: windows
+// end at n/32, n/16, n/8, n/4 and 3n/8 (whole multiples of b_outer), so the first one waits for 3 % of the
+// upload only and every later one finds its columns uploaded when the window before it is done.
+static int host_phase_bounds(mla_handle h, int64_t n, int b_outer, int64_t* out) {
+  int np = 0;
+  if (h->phase_count > 0) {
+    for (int i = 0; i < h->phase_count; ++i) {
+      int64_t c = h->phase_bounds[i] / b_outer * b_outer;
+      if (c > (np ? out[np - 1] : 0) && c < n) out[np++] = c;
+    }
+  } else if (h->phase_count < 0 && n >= 8192) {
+    const int64_t num[5] = {1, 2, 4, 8, 12};
+    for (int i = 0; i < 5; ++i) {
+      int64_t c = (n * num[i] / 32) / b_outer * b_outer;
+      if (c > (np ? out[np - 1] : 0) && c < n) out[np++] = c;
+    }
+  }
+  out[np++] = n;
+  return np;
+}
+
 extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_t ld_host,
                                  int32_t* ipiv_host, int b_outer, int b_inner, int variant, int sm_pf,
                                  int q_chunks, mla_lu_info* info_host) {
   if (!h || m < n || n < 0 || (m > 0 && ld_host < m)) return MLA_E_INVALID;
+  if (b_inner < 1 || b_outer < b_inner || b_outer > kMaxPiv) return MLA_E_INVALID;
   if (n == 0) { if (info_host) memset(info_host, 0, sizeof(*info_host)); return MLA_OK; }
   const int64_t ld = (m + 1) & ~(int64_t)1;   // even leading dimension: 16-byte aligned columns
   size_t bytes = (size_t)ld * (size_t)n * sizeof(double);
@@ -589,19 +653,39 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
     CK(h, cudaMalloc(&h->ipiv_dev, (size_t)n * sizeof(int32_t)));
     h->ipiv_dev_n = (size_t)n;
   }
-  // Upload, factor, and stream the result out WHILE the factorization runs: once an outer iteration
-  // has started with its panel at row q0, rows [0, q0) of the whole matrix are final (later
-  // interchanges, solves and updates only touch rows >= q0), so they are copied to the host as row
-  // blocks on a second stream.  The kernel reports q0 through a mapped host word.
+  // Upload, factor and download at the same time.
+  //  * Upload || factor: the columns travel in chunks on their own stream, and the factorization runs window by
+  //    window behind them (left-looking between windows): window [c0, c1) waits for its chunk only, is brought
+  //    up to date with the columns [0, c0) factored so far (catch_up: every interchange, then per 512-column
+  //    block a solve and a rank-512 update -- the operations an unwindowed run applies to these columns, in the
+  //    same order per entry, so the factors are the same bit for bit) and is then factored by the persistent
+  //    kernel restricted to it (look-ahead, WS and ET inside the window).  The last window takes everything left.
+  //  * Factor || download: once an outer iteration of the LAST window has started with its panel at row q0,
+  //    rows [0, q0) of the whole matrix are final (later interchanges, solves and updates only touch rows
+  //    >= q0), so they are copied to the host as row blocks on a second stream.  The kernel reports q0 through
+  //    a mapped host word.
   cudaStream_t s = h->s_main;
   *((volatile int*)h->progress_host) = 0;
-  CK(h, cudaMemcpy2DAsync(h->a_dev, ld * sizeof(double), A_host, ld_host * sizeof(double), m * sizeof(double), n,
-                          cudaMemcpyHostToDevice, s));
-  h->next_progress = h->progress_dev;
-  int rc = mla_getrf_la(h, h->a_dev, m, n, ld, h->ipiv_dev, b_outer, b_inner, variant, sm_pf, q_chunks, h->info_dev,
-                        nullptr, 0, s);
-  h->next_progress = nullptr;
-  if (rc != MLA_OK) return rc;
+  int64_t bounds[kMaxHostPhases];
+  const int np = host_phase_bounds(h, n, b_outer, bounds);
+  for (int g = 0; g < np; ++g) {
+    const int64_t c0 = g ? bounds[g - 1] : 0, c1 = bounds[g];
+    CK(h, cudaMemcpy2DAsync(h->a_dev + c0 * ld, ld * sizeof(double), A_host + c0 * ld_host, ld_host * sizeof(double),
+                            m * sizeof(double), c1 - c0, cudaMemcpyHostToDevice, h->s_up));
+    CK(h, cudaEventRecord(h->ev_up[g], h->s_up));
+  }
+  for (int g = 0; g < np; ++g) {
+    const int64_t c0 = g ? bounds[g - 1] : 0, c1 = bounds[g];
+    CK(h, cudaStreamWaitEvent(s, h->ev_up[g], 0));
+    int rc = MLA_OK;
+    if (c0 > 0) rc = catch_up(h, h->a_dev, m, ld, h->ipiv_dev, c0, c0, c1, b_outer, h->phase_deep != 0, s);
+    if (rc != MLA_OK) return rc;
+    h->next_progress = (g == np - 1) ? h->progress_dev : nullptr;
+    rc = getrf_launch(h, h->a_dev, m, c1, ld, h->ipiv_dev, b_outer, b_inner, variant, sm_pf, q_chunks, h->info_dev,
+                      nullptr, 0, c0, s);
+    h->next_progress = nullptr;
+    if (rc != MLA_OK) return rc;
+  }
   CK(h, cudaEventRecord(h->ev_done, s));
   const int64_t min_rows = 512;   // row blocks of 128 ... 2048 rows were measured: no difference beyond noise
   int64_t done_rows = 0;
@@ -623,7 +707,7 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
   CK(h, cudaMemcpyAsync(ipiv_host, h->ipiv_dev, n * sizeof(int32_t), cudaMemcpyDeviceToHost, h->s_copy));
   CK(h, cudaMemcpyAsync(h->info_host, h->info_dev, sizeof(mla_lu_info), cudaMemcpyDeviceToHost, h->s_copy));
   CK(h, cudaStreamSynchronize(h->s_copy));
-  rc = check_abort(h, s);
+  int rc = check_abort(h, s);
   if (info_host) *info_host = *h->info_host;
   return rc;
 }
@@ -643,13 +727,16 @@ struct ApplyArgs {
   double* L; int64_t ldl; int left_cols;   // columns LEFT of the panel (interchanges only; nullable)
   PivPlan* plan; unsigned* ctrl; unsigned* flags; unsigned tag;
   const DiagInv* inv;       // inverted diagonal blocks of the panel's unit-lower top block (mla_apply_panel_prepare)
+  // catch-up steps of the phased host entry point (left-looking: every interchange was applied up front):
+  int no_swaps;             // 1: the strips skip the interchanges (no plan is read)
+  int gemm_rows;            // the rank-w update stops at this row of the view (== rows: the whole height)
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
   extern __shared__ __align__(16) double smem[];
   const int nstrips = (a.cols + TRSM_CW - 1) / TRSM_CW;
   const int nleft = (a.left_cols + LEFT_CW - 1) / LEFT_CW;
-  const int rows_below = a.rows - a.w;
+  const int rows_below = a.gemm_rows - a.w;
   const int tmc = (rows_below + GemmUpdateCfg::BM - 1) / GemmUpdateCfg::BM;
   const int first_gemm = nstrips + nleft;
   const int total = first_gemm + nstrips * tmc;
@@ -667,11 +754,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
     const int c0 = strip * TRSM_CW, i0 = a.w + tm * GemmUpdateCfg::BM;
     double* c = a.T + (int64_t)c0 * a.ldt + i0;
     return TileDesc{a.P + i0, a.ldp, a.T + (int64_t)c0 * a.ldt, a.ldt, c, a.ldt, c, a.ldt,
-                    a.w, a.rows - i0, imin(TRSM_CW, a.cols - c0), 1.0, -1.0, true};
+                    a.w, a.gemm_rows - i0, imin(TRSM_CW, a.cols - c0), 1.0, -1.0, true};
   };
   // a pivot index out of range (k_laswp_plan's verdict): nothing may be touched, and the caller must
   // hear about it -- the abort word is what the asynchronous entry points report (mla_abort_word)
-  if (*((volatile unsigned*)(a.ctrl + CW_ERR_INDEX)) != 0u) {
+  if (!a.no_swaps && *((volatile unsigned*)(a.ctrl + CW_ERR_INDEX)) != 0u) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.ctrl + CW_ABORT, 0xBAD1u);
     return;
   }
@@ -689,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_apply_panel(ApplyArgs a) {
       // columns below skip_cols are the leftover of an ET-cut panel and already hold both
       const int c0 = t * TRSM_CW, c1 = imin(a.cols, c0 + TRSM_CW), lo = imax(c0, a.skip_cols);
       if (lo < c1) {
-        laswp_apply_cols(a.T + (int64_t)lo * a.ldt, a.ldt, c1 - lo, a.plan->ref(), smem, kLaswpBufDoubles);
+        if (!a.no_swaps) laswp_apply_cols(a.T + (int64_t)lo * a.ldt, a.ldt, c1 - lo, a.plan->ref(), smem, kLaswpBufDoubles);
         if (trsm_use_inverse(a.w)) trsm_strip_inv(a.P, a.w, a.ldp, a.T + (int64_t)lo * a.ldt, c1 - lo, a.ldt, a.inv, smem);
         else trsm_strip_ool(a.P, a.w, a.ldp, a.T + (int64_t)lo * a.ldt, c1 - lo, a.ldt, smem);
       }
@@ -772,7 +859,7 @@ extern "C" int mla_apply_panel_launch(mla_handle h, const double* P, int64_t row
   cudaStream_t s = (cudaStream_t)stream;
   CK(h, cudaFuncSetAttribute(k_apply_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
   ApplyArgs a{P, ldp, (int)rows, (int)w, T, ldt, (int)cols, (int)(skip_cols < cols ? skip_cols : cols), L, ldl,
-              (int)left_cols, h->plan, h->ctrl, h->lu_state->rprep_done, h->apply_tag, h->dinv};
+              (int)left_cols, h->plan, h->ctrl, h->lu_state->rprep_done, h->apply_tag, h->dinv, 0, (int)rows};
   void* args[] = {&a};
   int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
   if (h->update_sms > 0 && h->update_sms < grid) grid = h->update_sms;
@@ -789,6 +876,38 @@ extern "C" int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int6
   int rc = mla_apply_panel_prepare(h, P, ldp, ipiv, w, rows, stream);
   if (rc != MLA_OK) return rc;
   return mla_apply_panel_launch(h, P, rows, w, ldp, T, cols, ldt, 0, nullptr, 0, 0, 0, stream);
+}
+
+// Left-looking catch-up of the phased host entry point: columns [c0, c1) of the m-row matrix A have seen nothing
+// of the factorization so far; columns [0, k), k <= c0, are factored (unit-lower L below / U above the diagonal,
+// global pivots in ipiv).  All k interchanges first (the L rows are already in their final order, so the new
+// columns must be brought into it before any row of L meets them), then per b_outer-column block [p0, p0 + w)
+// the solve with its unit-lower diagonal block and the rank-w update of the rows below -- one k_apply_panel
+// launch each, without interchanges.  deep: those updates stop at row k and the rows below get ONE multiply of
+// depth k instead (C is then read and written once per window, not once per block).
+static int catch_up(mla_handle h, double* A, int64_t m, int64_t ld, const int32_t* ipiv, int64_t k, int64_t c0,
+                    int64_t c1, int b_outer, bool deep, cudaStream_t s) {
+  if (k <= 0 || c1 <= c0) return MLA_OK;
+  int rc = laswp_impl(h, A + c0 * ld, m, c1 - c0, ld, ipiv, k, 0, (void*)s, false);
+  if (rc != MLA_OK) return rc;
+  CK(h, cudaFuncSetAttribute(k_apply_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
+  const int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
+  for (int64_t p0 = 0; p0 < k; p0 += b_outer) {
+    const int64_t w = k - p0 < b_outer ? k - p0 : b_outer;
+    const double* P = A + p0 * ld + p0;
+    const int64_t rows = m - p0;
+    if (trsm_use_inverse((int)w)) { rc = launch_diag_inv(h, P, w, ld, h->dinv, s); if (rc != MLA_OK) return rc; }
+    CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
+    CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_DONE, 0, sizeof(unsigned), s));
+    ++h->apply_tag;
+    ApplyArgs a{P, ld, (int)rows, (int)w, A + c0 * ld + p0, ld, (int)(c1 - c0), 0, nullptr, 0, 0, h->plan, h->ctrl,
+                h->lu_state->rprep_done, h->apply_tag, h->dinv, 1, (int)(deep ? k - p0 : rows)};
+    void* args[] = {&a};
+    CK(h, cudaLaunchCooperativeKernel((void*)k_apply_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
+  }
+  if (deep && m > k)
+    return mla_gemm(h, A + c0 * ld + k, m - k, c1 - c0, ld, A + k, ld, A + c0 * ld, ld, k, 1.0, -1.0, nullptr, 0, (void*)s);
+  return MLA_OK;
 }
 
 extern "C" int mla_step_flag(mla_handle h, uint32_t** flag_dev, uint32_t* tag) {

@@ -456,13 +456,16 @@ __device__ __forceinline__ TileDesc gemm_tile_desc(const GemmProblem& p, int t) 
   // tiles go strip by strip.  The A rows of one block (kRowBlockTiles x BM x k doubles, 16 MiB at
   // k = 256) then stay in L2 while every column strip passes over them, instead of the whole m x k
   // operand being re-read from HBM for every strip.
+  // Deep multiplies (k > 512: the catch-up updates of the phased host entry point) shrink the block so that
+  // its A rows still fit L2: rbt * BM * k * 8 bytes <= 32 MiB, at least 4 row tiles.
+  const int rbt = imax(4, imin(kRowBlockTiles, (kRowBlockTiles * 512) / imax(p.k, 1)));
   const int tm_count = (p.m + Cfg::BM - 1) / Cfg::BM;
   const int tn_count = (p.n + Cfg::BN - 1) / Cfg::BN;
-  const int per_block = kRowBlockTiles * tn_count;
+  const int per_block = rbt * tn_count;
   const int rb = t / per_block;
-  const int rows_here = imin(kRowBlockTiles, tm_count - rb * kRowBlockTiles);
+  const int rows_here = imin(rbt, tm_count - rb * rbt);
   const int r = t - rb * per_block;
-  const int tn = r / rows_here, tm = rb * kRowBlockTiles + (r - tn * rows_here);
+  const int tn = r / rows_here, tm = rb * rbt + (r - tn * rows_here);
   const int i0 = tm * Cfg::BM, j0 = tn * Cfg::BN;
   double* c = p.C + (int64_t)j0 * p.ldc + i0;
   return TileDesc{p.A + i0, p.lda, p.B + (int64_t)j0 * p.ldb, p.ldb, c, p.ldc, c, p.ldc,

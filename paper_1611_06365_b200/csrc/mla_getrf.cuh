@@ -99,6 +99,11 @@ struct GetrfArgs {
   int* widths; int widths_cap;
   TraceEv* tr;               // per-CTA event rings (kTraceEvPerCta records each) of the TRACED kernel, else unused
   DiagInv* dinv;             // two sets of inverted diagonal blocks: iteration `it` solves with set it & 1
+  // Windowed run (the phased host entry point): columns [0, k0) are already factored and applied to columns
+  // [k0, n); this launch factors columns [k0, n) of the m-row matrix, its interchanges reach back over the
+  // columns left of k0 (LEFT items), and the outcome counters / iteration numbering in LuState carry on from
+  // the previous launch (the host does not reset LuState).  k0 == 0: a fresh factorization.
+  int k0;
 };
 
 // item counts of one iteration, derived identically by every CTA from the descriptor
@@ -500,11 +505,24 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
   const int m = a.m, n = a.n;
   const bool dbgk = (bid == G - 1) && tid == 0;
 
+  const int k0 = a.k0;
   if (tid == 0) {
     ks.all_target = 0u; ks.pf_target = 0u; ks.ok = 1; ks.sm_pf = sm_pf_lo;
-    ks.k_new = 0; ks.w_sched = 0; ks.q1_of_panel = 0; ks.b_target = a.b_outer; ks.singular = 0; ks.et_events = 0;
-    ks.n_panels = 0; ks.ws_joins = 0; ks.q0 = 0; ks.q1 = 0; ks.it_next = 1; ks.prebuilt = 0;
+    ks.k_new = 0; ks.w_sched = 0; ks.q1_of_panel = k0; ks.b_target = a.b_outer; ks.singular = 0; ks.et_events = 0;
+    ks.n_panels = 0; ks.ws_joins = 0; ks.q0 = k0; ks.q1 = k0; ks.it_next = 1; ks.prebuilt = 0;
     ks.t_iter0 = 0ull; ks.tr_n = 0; ks.tr_t0 = 0ull;
+    if (k0 > 0) {
+      // resume: nobody writes LuState before the prologue panel's collective has been entered by every CTA
+      ks.singular = *((volatile const int*)&st->singular); ks.et_events = *((volatile const int*)&st->et_events);
+      ks.n_panels = *((volatile const int*)&st->n_panels); ks.ws_joins = *((volatile const int*)&st->ws_joins);
+      ks.it_next = *((volatile const int*)&st->it) + 1;
+      if constexpr (TRACE) {
+        // the CTA's event ring carries on behind the records of the earlier windows
+        int used = 0;
+        while (used < kTraceEvPerCta && a.tr[(size_t)bid * kTraceEvPerCta + used].kind != 0) ++used;
+        ks.tr_n = used;
+      }
+    }
   }
   if (tid < 8) g_dbg[tid] = 0ull;
   __syncthreads();
@@ -541,16 +559,35 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
   };
 
   // ---- prologue: first panel, the whole grid as one team (lu.py:224-241) --------------------------
+  // (a later window's first panel is factored by the panel team instead, like the look-ahead panel it would
+  // have been in an unwindowed run: the factors then do not depend on where the windows are cut)
   {
-    const int w0 = imin(a.b_outer, n);
-    tr_begin();
-    Team t = team_all();
-    PanelResult pr = panel_ll(t, a.A, m, w0, a.ld, a.piv_local, a.b_inner, nullptr, 0u, 0, a.pws, smem, smem_doubles, true);
-    keep_panel_result(pr);
-    if (tid == 0) ks.w_sched = w0;
-    put_all(t);
-    invert_diag_blocks(a.A, pr.cols_factored, bid, G, 1);
-    tr_end(TK_PANEL_ALL, 0, pr.cols_factored, G);
+    const int w0 = imin(a.b_outer, n - k0);
+    double* const P0 = a.A + (int64_t)k0 * a.ld + k0;
+    const int it_first = ks.it_next;
+    if (k0 > 0 && la) {
+      if (bid < ks.sm_pf) {
+        tr_begin();
+        Team t = team_pf();
+        PanelResult pr = panel_ll(t, P0, m - k0, w0, a.ld, a.piv_local, a.b_inner, nullptr, 0u, 0, a.pws, smem, smem_doubles, true);
+        keep_panel_result(pr);
+        const bool pf_ok = t.ok;
+        put_pf(t);
+        if (pf_ok) invert_diag_blocks(P0, pr.cols_factored, bid, ks.sm_pf, it_first);
+        tr_end(TK_PANEL, it_first - 1, pr.cols_factored, ks.sm_pf);
+      }
+      if (tid == 0) ks.w_sched = w0;
+      __syncthreads();
+    } else {
+      tr_begin();
+      Team t = team_all();
+      PanelResult pr = panel_ll(t, P0, m - k0, w0, a.ld, a.piv_local, a.b_inner, nullptr, 0u, 0, a.pws, smem, smem_doubles, true);
+      keep_panel_result(pr);
+      if (tid == 0) ks.w_sched = w0;
+      put_all(t);
+      invert_diag_blocks(P0, pr.cols_factored, bid, G, it_first);
+      tr_end(TK_PANEL_ALL, it_first - 1, pr.cols_factored, G);
+    }
   }
   if (dbgk) ks.k_t0 = globaltimer_ns();
 
@@ -574,7 +611,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
         if (a.widths && n_panels < a.widths_cap) a.widths[n_panels] = k_new;
         ++n_panels;
         if (k_new < w_sched) { ++et_events; b_target = imax(a.b_inner, k_new); }
-        else if (q1_of_panel > 0) b_target = imin(a.b_outer, 2 * b_target);
+        else if (q1_of_panel > k0) b_target = imin(a.b_outer, 2 * b_target);
         const int pend = q1_of_panel + w_sched;
         const int q0 = q1_of_panel, q1 = q1_of_panel + k_new;
         ks.q0 = q0; ks.q1 = q1; ks.b_target = b_target; ks.n_panels = n_panels; ks.et_events = et_events;
@@ -592,7 +629,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
         st->pq_next = 0; st->pq_done = 0; st->rq_next = 0; st->rq_done = 0;
         if (la) {
           int T = ks.sm_pf;
-          if (sm_pf_hi > sm_pf_lo && q1_of_panel > 0) {
+          if (sm_pf_hi > sm_pf_lo && q1_of_panel > k0) {
             const unsigned long long pe = *((volatile unsigned long long*)&st->t_panel_end);
             const unsigned long long rd = *((volatile unsigned long long*)&st->t_rq_done);
             if (rd == 0ull || pe > rd) T = imin(sm_pf_hi, 2 * T);
@@ -724,7 +761,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
   }
   if (dbgk) {
     g_dbg[6] += globaltimer_ns() - ks.k_t0;
-    for (int i = 0; i < 8; ++i) st->dbg[i] = g_dbg[i];
+    for (int i = 0; i < 8; ++i) st->dbg[i] = (k0 > 0 ? st->dbg[i] : 0ull) + g_dbg[i];
   }
   if (bid == 0 && tid == 0 && a.info) {
     a.info->cols_factored = n;
