@@ -170,6 +170,23 @@ int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_
  * window; same result up to rounding, no longer bit-identical). */
 int mla_set_host_phases(mla_handle h, const int64_t* bounds, int count, int deep);
 
+/* Windowed (two-level) factorization, used by mla_getrf_la* for n >= min_n (default: width 4096, min_n 16384).
+ * The columns are cut into windows of `width` columns (rounded down to a whole multiple of b_outer).  A window is
+ * factored by the persistent kernel restricted to it -- lu_la's look-ahead / WS / ET schedule of lu.py:243-326
+ * with the panels clamped to the window, the same rule the multi-GPU layout uses for its column blocks -- and then
+ * applied to the columns on its right: interchanges, per b_outer block the solve and the rank-b update down to the
+ * window's end, and ONE multiply of depth `width` for all rows below (C is read and written once per window
+ * instead of once per panel: 34-35 TFLOP/s).  That multiply is done at once for the next window's own columns; for
+ * the others it becomes the FILLER of the next window's persistent kernel: update-team CTAs that have drained
+ * their queue execute 128 x 128 x 1024 units of it instead of waiting for the panel (the idle time WS and ET
+ * attack from the panel's side, lu.py:305-312).  The result does not depend on the timing (every entry sees the
+ * same additions in the same order); the width schedule can be replayed on the CPU oracle with clamp = width.
+ * In mla_getrf_la_host the same operations are scheduled behind the upload: window-sized column chunks (the first
+ * window cut once more at first_chunk columns), a window is applied to the columns that are on the device, a chunk
+ * that arrives later first receives every window it missed, in the same order -- so the factors are bit-identical
+ * to mla_getrf_la's for the variants without ET.  width == 0 switches windows off (one persistent launch). */
+int mla_set_windows(mla_handle h, int width, int64_t min_n, int first_chunk);
+
 /* One update step of the multi-GPU driver as a single persistent launch: apply the broadcast panel P
  * (rows x w: unit-lower L11 on top of L21, leading dimension ldp) with its w panel-local pivots to the
  * column block T (rows x cols view starting at the panel's first row):

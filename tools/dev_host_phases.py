@@ -66,12 +66,11 @@ def timing(n):
     host_t = a.t().contiguous().cpu().pin_memory()          # (n, n): rows are the matrix's columns
     del a
     work = torch.empty_like(host_t).pin_memory()
-    layouts = [("one phase", [], 0), ("default", None, 0), ("default deep", None, 1)]
     f = n // 32
-    layouts += [("n/32 n/16 n/8 n/4", [f, 2 * f, 4 * f, 8 * f], 0), ("n/32 n/16 n/8 n/4 deep", [f, 2 * f, 4 * f, 8 * f], 1),
-                ("n/32 n/8 3n/8 deep", [f, 4 * f, 12 * f], 1), ("n/16 n/4 deep", [2 * f, 8 * f], 1),
-                ("n/32..n/2 deep", [f, 2 * f, 4 * f, 8 * f, 12 * f, 16 * f], 1)]
-    for variant in ("lu_et",):
+    layouts = [("one phase", [], 0), ("n/32 n/8 3n/8", [f, 4 * f, 12 * f], 0), ("n/32 n/8 3n/8 deep", [f, 4 * f, 12 * f], 1),
+               ("n/32 n/8 n/4 deep", [f, 4 * f, 8 * f], 1), ("n/32 3n/32 n/4 deep", [f, 3 * f, 8 * f], 1),
+               ("n/32 n/8 n/2 deep", [f, 4 * f, 16 * f], 1)]
+    for variant in VARIANTS:
         for name, bounds, deep in layouts:
             set_phases(bounds, deep)
             ts = []
@@ -81,6 +80,8 @@ def timing(n):
                 if i: ts.append(dt)
             print(f"n={n} {variant} {name}: {np.mean(ts)*1e3:.1f} ms (min {min(ts)*1e3:.1f}), panels {info.n_panels}, et {info.et_events}", flush=True)
     set_phases(None)
+
+VARIANTS = tuple(os.environ.get("VARIANTS", "lu_et,lu_mb").split(","))
 
 if __name__ == "__main__":
     args = sys.argv[1:] or ["check"]
