@@ -159,33 +159,19 @@ int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_
 
 /* Windows of mla_getrf_la_host (the upload is overlapped too): the columns are uploaded in chunks and the
  * factorization runs window by window behind the upload, left-looking between windows -- window [c0, c1) waits
- * for its own chunk only, receives the interchanges / solves / rank-b updates of the columns [0, c0) factored so
- * far, and is then factored by the persistent kernel restricted to it (look-ahead, WS and ET inside the window;
- * lu_la's own iteration structure, lu.py:243-326, from column c0 on).  Every matrix entry sees the same operations
- * in the same order as in an unwindowed run, so for the variants without ET the factors are bit-identical to
- * mla_getrf_la's.  bounds/count: window ends in columns, ascending (rounded down to whole multiples of b_outer;
- * the last window always ends at n); count == 0: one window (upload, then factor); count < 0 (default): windows
- * end at n/32, n/16, n/8, n/4, 3n/8 for n >= 8192.  deep != 0: the catch-up of a window updates the rows below
- * the factored block with ONE multiply of depth c0 instead of one rank-b update per block (fewer passes over the
- * window; same result up to rounding, no longer bit-identical). */
+ * for its own chunk only, receives the interchanges / solves / updates of the columns [0, c0) factored so far
+ * (catch-up), and is then factored by the persistent kernel restricted to it (look-ahead, WS and ET inside the
+ * window; lu_la's own iteration structure, lu.py:243-326, from column c0 on).
+ *   bounds/count: window ends in columns, ascending (rounded down to whole multiples of b_outer; the last window
+ *          always ends at n); count == 0: one window (upload, then factor); count < 0 (default): windows end at
+ *          n/32, n/8 and 3n/8 for n >= 8192.
+ *   deep:  0: the catch-up applies one b_outer block at a time (solve + rank-b update of all rows below) -- every
+ *          matrix entry then sees the same operations in the same order as in an unwindowed run, and for the
+ *          variants without ET the factors are bit-identical to mla_getrf_la's;
+ *          > 0 (default 4096): the factored columns are taken in super-blocks of `deep` columns, the rank-b updates
+ *          stop at the super-block's last row and the rows below get ONE multiply of depth `deep` per super-block
+ *          (34-35 TFLOP/s; same pivots, factors equal up to rounding). */
 int mla_set_host_phases(mla_handle h, const int64_t* bounds, int count, int deep);
-
-/* Windowed (two-level) factorization, used by mla_getrf_la* for n >= min_n (default: width 4096, min_n 16384).
- * The columns are cut into windows of `width` columns (rounded down to a whole multiple of b_outer).  A window is
- * factored by the persistent kernel restricted to it -- lu_la's look-ahead / WS / ET schedule of lu.py:243-326
- * with the panels clamped to the window, the same rule the multi-GPU layout uses for its column blocks -- and then
- * applied to the columns on its right: interchanges, per b_outer block the solve and the rank-b update down to the
- * window's end, and ONE multiply of depth `width` for all rows below (C is read and written once per window
- * instead of once per panel: 34-35 TFLOP/s).  That multiply is done at once for the next window's own columns; for
- * the others it becomes the FILLER of the next window's persistent kernel: update-team CTAs that have drained
- * their queue execute 128 x 128 x 1024 units of it instead of waiting for the panel (the idle time WS and ET
- * attack from the panel's side, lu.py:305-312).  The result does not depend on the timing (every entry sees the
- * same additions in the same order); the width schedule can be replayed on the CPU oracle with clamp = width.
- * In mla_getrf_la_host the same operations are scheduled behind the upload: window-sized column chunks (the first
- * window cut once more at first_chunk columns), a window is applied to the columns that are on the device, a chunk
- * that arrives later first receives every window it missed, in the same order -- so the factors are bit-identical
- * to mla_getrf_la's for the variants without ET.  width == 0 switches windows off (one persistent launch). */
-int mla_set_windows(mla_handle h, int width, int64_t min_n, int first_chunk);
 
 /* One update step of the multi-GPU driver as a single persistent launch: apply the broadcast panel P
  * (rows x w: unit-lower L11 on top of L21, leading dimension ldp) with its w panel-local pivots to the

@@ -84,8 +84,6 @@ def lib() -> ctypes.CDLL:
     L.mla_set_update_sms.restype = ctypes.c_int
     L.mla_set_host_phases.argtypes = [_vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int, ctypes.c_int]
     L.mla_set_host_phases.restype = ctypes.c_int
-    L.mla_set_windows.argtypes = [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int]
-    L.mla_set_windows.restype = ctypes.c_int
     L.mla_set_panel_sms_max.argtypes = [_vp, ctypes.c_int]
     L.mla_set_panel_sms_max.restype = ctypes.c_int
     L.mla_getrf_debug.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64)]
@@ -106,7 +104,7 @@ EXPORTS = ("mla_version", "mla_create", "mla_destroy", "mla_num_sms", "mla_last_
            "mla_apply_panel", "mla_set_panel_sms_max", "mla_panel_ll_async",
            "mla_set_update_sms", "mla_apply_panel_prepare", "mla_apply_panel_launch", "mla_abort_word",
            "mla_step_flag", "mla_set_trace", "mla_getrf_events", "mla_pack_panel", "mla_packed_panel_doubles", "mla_release_host_cache",
-           "mla_set_host_phases", "mla_set_windows")
+           "mla_set_host_phases")
 
 
 class MlaError(RuntimeError):

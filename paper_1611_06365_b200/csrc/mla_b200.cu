@@ -7,7 +7,6 @@
 #include <cstring>
 #include <thread>
 #include <new>
-#include <vector>
 
 #include "../../include/mla_b200.h"
 #include "mla_common.cuh"
@@ -16,7 +15,6 @@
 #include "mla_trsm.cuh"
 #include "mla_panel.cuh"
 #include "mla_getrf.cuh"
-#include "mla_filler.cuh"
 
 using namespace mla;
 
@@ -35,9 +33,6 @@ enum CtrlWord {
 constexpr int kDynSmemBytes = 218 * 1024;   // dynamic shared memory of the team kernels
 constexpr int kDynSmemDoubles = kDynSmemBytes / 8;
 constexpr int kMaxHostPhases = 16;
-constexpr int kDefaultWindow = 4096;          // window width of the two-level factorization
-constexpr int64_t kDefaultWindowMinN = 16384; // ... used from this many columns on
-constexpr int kFillerChunk = 1024;            // k depth of one filler unit
 
 struct mla_handle_s {
   int device;
@@ -72,16 +67,7 @@ struct mla_handle_s {
   cudaEvent_t ev_up[kMaxHostPhases];
   int phase_count;       // -1: default policy, 0: one phase (upload, then factor), > 0: explicit boundaries
   int64_t phase_bounds[kMaxHostPhases];
-  int phase_deep;        // 1: catch-up updates as one deep multiply per window instead of one per panel
-  // windowed (two-level) factorization: window width (0 = off), smallest n it is used for, first upload chunk
-  int win_width;
-  int64_t win_min_n;
-  int win_first_chunk;
-  FillerQ* fill_dev;     // device: the one filler queue (stream-ordered reuse)
-  unsigned* fill_prog;   // device: per-tile chunk counters of the filler queue
-  size_t fill_prog_n;
-  std::vector<cudaEvent_t>* up_events;   // one event per uploaded column chunk (windowed host entry point)
-  cudaEvent_t ev_stage;
+  int phase_deep;        // > 0: catch-up in super-blocks of this many columns, one deep multiply each (0: per panel)
 };
 
 #define CK(h, call)                                   \
@@ -128,13 +114,8 @@ extern "C" int mla_create(int device, mla_handle* out) {
   for (int i = 0; ok && i < kMaxHostPhases; ++i)
     ok = cudaEventCreateWithFlags(&h->ev_up[i], cudaEventDisableTiming) == cudaSuccess;
   h->phase_count = -1;
-  h->win_width = kDefaultWindow;
-  h->win_min_n = kDefaultWindowMinN;
-  h->win_first_chunk = 1024;
-  ok = ok && cudaMalloc(&h->fill_dev, sizeof(FillerQ)) == cudaSuccess &&
-       cudaEventCreateWithFlags(&h->ev_stage, cudaEventDisableTiming) == cudaSuccess;
-  h->up_events = new (std::nothrow) std::vector<cudaEvent_t>();
-  if (!ok || !h->up_events) { mla_destroy(h); return MLA_E_NOMEM; }
+  h->phase_deep = 4096;
+  if (!ok) { mla_destroy(h); return MLA_E_NOMEM; }
   cudaMemset(h->plan, 0, 2 * sizeof(PivPlan));
   cudaMemset(h->panel_ws, 0, sizeof(PanelWs));
   cudaMemset(h->lu_state, 0, sizeof(LuState));
@@ -162,10 +143,6 @@ extern "C" int mla_destroy(mla_handle h) {
   if (h->s_main) cudaStreamDestroy(h->s_main);
   if (h->s_copy) cudaStreamDestroy(h->s_copy);
   if (h->s_up) cudaStreamDestroy(h->s_up);
-  cudaFree(h->fill_dev);
-  cudaFree(h->fill_prog);
-  if (h->ev_stage) cudaEventDestroy(h->ev_stage);
-  if (h->up_events) { for (cudaEvent_t e : *h->up_events) cudaEventDestroy(e); delete h->up_events; }
   for (int i = 0; i < kMaxHostPhases; ++i) if (h->ev_up[i]) cudaEventDestroy(h->ev_up[i]);
   if (h->ev_done) cudaEventDestroy(h->ev_done);
   if (h->progress_host) cudaFreeHost(h->progress_host);
@@ -367,7 +344,7 @@ k_laswp_apply(double* A, int64_t cols, int64_t ld, PivPlan* plan) {
 }
 
 static int laswp_impl(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
-                      int64_t npiv, int reverse, void* stream, bool readback, int64_t t_first = 0);
+                      int64_t npiv, int reverse, void* stream, bool readback);
 
 extern "C" int mla_laswp(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
                          int64_t npiv, int reverse, void* stream) {
@@ -379,12 +356,10 @@ extern "C" int mla_laswp_async(mla_handle h, double* A, int64_t rows, int64_t co
   return laswp_impl(h, A, rows, cols, ld, ipiv, npiv, reverse, stream, false);
 }
 
-// t_first > 0 (forward only): only the interchanges [t_first, npiv) of the vector are applied
 static int laswp_impl(mla_handle h, double* A, int64_t rows, int64_t cols, int64_t ld, const int32_t* ipiv,
-                      int64_t npiv, int reverse, void* stream, bool readback, int64_t t_first) {
-  if (!h || rows < 0 || cols < 0 || npiv < 0 || (rows > 0 && ld < rows) || t_first < 0 || (t_first > 0 && reverse))
-    return MLA_E_INVALID;
-  if (npiv <= t_first) return MLA_OK;
+                      int64_t npiv, int reverse, void* stream, bool readback) {
+  if (!h || rows < 0 || cols < 0 || npiv < 0 || (rows > 0 && ld < rows)) return MLA_E_INVALID;
+  if (npiv == 0) return MLA_OK;
   if (!ipiv || rows >= (1ll << 31)) return MLA_E_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   const int smem_bytes = kLaswpBufDoubles * 8;
@@ -392,15 +367,15 @@ static int laswp_impl(mla_handle h, double* A, int64_t rows, int64_t cols, int64
   // Pivot vectors longer than one plan (kMaxPiv) are applied as consecutive chunks of the SAME view
   // (ascending for forward, descending for reverse); the whole vector is range-checked on the device
   // first, and a bad index anywhere empties every chunk's plan, so nothing is touched.
-  const int64_t nchunks = (npiv - t_first + kMaxPiv - 1) / kMaxPiv;
-  const int preval = (nchunks > 1 || t_first > 0) ? 1 : 0;
+  const int64_t nchunks = (npiv + kMaxPiv - 1) / kMaxPiv;
+  const int preval = nchunks > 1 ? 1 : 0;
   if (preval) {
     k_laswp_validate<<<1, 256, 0, s>>>(ipiv, npiv, rows, h->ctrl);
     CK(h, cudaGetLastError());
   }
   for (int64_t ci = 0; ci < nchunks; ++ci) {
     const int64_t c = reverse ? (nchunks - 1 - ci) : ci;
-    const int64_t t0 = t_first + c * kMaxPiv;
+    const int64_t t0 = c * kMaxPiv;
     const int np = (int)(npiv - t0 < kMaxPiv ? npiv - t0 : kMaxPiv);
     k_laswp_plan<<<1, 32, 0, s>>>(ipiv + t0, np, rows, reverse, (int)t0, preval, h->plan, h->ctrl);
     CK(h, cudaGetLastError());
@@ -530,45 +505,19 @@ int mla_launch_getrf_traced(const GetrfArgs& a, int grid, int smem_bytes, cudaSt
 
 // One launch of the persistent kernel: columns [k0, n) of the m-row matrix (k0 > 0: a later window of the phased
 // host entry point -- columns [0, k0) are factored and applied, LuState carries on, a raised abort word stays).
-struct LuParams {          // what every launch of one factorization shares
-  double* A; int64_t m, n, ld; int32_t* ipiv;
-  int b_outer, b_inner, variant, sm_pf, q_chunks;
-  mla_lu_info* info_dev; int32_t* widths; int widths_cap;
-};
-struct UploadCtx;          // host entry point only: the column chunks still travelling to the device
 static int getrf_launch(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
                         int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
-                        int32_t* widths, int widths_cap, int64_t k0, void* stream, FillerQ* fill = nullptr,
-                        int64_t progress_cap = (1ll << 30), int64_t left_skip0 = 0, int64_t left_skip1 = 0);
-static int getrf_windowed(mla_handle h, const LuParams& p, UploadCtx* up, cudaStream_t s);
-// window width actually used: a whole multiple of b_outer and of the LEFT item width (0: no windows)
-static int64_t window_width(mla_handle h, int b_outer) {
-  if (b_outer < 1 || h->win_width < b_outer) return 0;
-  int64_t w = (int64_t)h->win_width / b_outer * b_outer;
-  while (w > 0 && w % LEFT_CW) w -= b_outer;
-  return w;
-}
-static bool use_windows(mla_handle h, int64_t n, int b_outer) {
-  const int64_t w = window_width(h, b_outer);
-  return w > 0 && n >= h->win_min_n && n > w;
-}
+                        int32_t* widths, int widths_cap, int64_t k0, void* stream);
 
 extern "C" int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
                             int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
                             int32_t* widths, int widths_cap, void* stream) {
-  if (h && b_outer >= 1 && use_windows(h, n, b_outer) && !h->next_progress) {
-    LuParams p{A, m, n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks, info_dev, widths, widths_cap};
-    return getrf_windowed(h, p, nullptr, (cudaStream_t)stream);
-  }
   return getrf_launch(h, A, m, n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks, info_dev, widths, widths_cap, 0, stream);
 }
 
 static int getrf_launch(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
                         int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
-                        int32_t* widths, int widths_cap, int64_t k0, void* stream, FillerQ* fill,
-                        int64_t progress_cap, int64_t left_skip0, int64_t left_skip1) {
-  if (left_skip1 > left_skip0 && (left_skip0 % LEFT_CW || left_skip1 % LEFT_CW || left_skip1 > k0 || left_skip0 < 0))
-    return MLA_E_INVALID;
+                        int32_t* widths, int widths_cap, int64_t k0, void* stream) {
   if (!h || m < n || n < 0 || (m > 0 && ld < m) || k0 < 0 || (k0 > 0 && k0 >= n)) return MLA_E_INVALID;
   if (b_inner < 1 || b_outer < b_inner || b_outer > kMaxPiv) return MLA_E_INVALID;
   if (variant < MLA_VARIANT_LU || variant > MLA_VARIANT_LU_ET) return MLA_E_INVALID;
@@ -589,8 +538,7 @@ static int getrf_launch(mla_handle h, double* A, int64_t m, int64_t n, int64_t l
   }
   GetrfArgs a{A, (int)m, (int)n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks < 1 ? 1 : q_chunks,
               h->sm_pf_max, h->next_progress, h->lu_state, h->plan, h->panel_ws, h->piv_local, h->ctrl, info_dev, widths, widths_cap,
-              h->trace_dev, h->dinv, (int)k0, (int)(progress_cap < (1ll << 30) ? progress_cap : (1ll << 30)), fill,
-              (int)left_skip0, (int)(left_skip1 > left_skip0 ? left_skip1 : left_skip0)};
+              h->trace_dev, h->dinv, (int)k0};
   h->next_progress = nullptr;
   int e = h->trace_dev ? mla_launch_getrf_traced(a, grid, kDynSmemBytes, s) : mla_launch_getrf(a, grid, kDynSmemBytes, s);
   if (e != 0) { h->last_cuda = e; return MLA_E_CUDA; }
@@ -655,18 +603,7 @@ extern "C" int mla_release_host_cache(mla_handle h) {
 }
 
 static int catch_up(mla_handle h, double* A, int64_t m, int64_t ld, const int32_t* ipiv, int64_t k, int64_t c0,
-                    int64_t c1, int b_outer, bool deep, cudaStream_t s);
-struct UploadCtx {
-  std::vector<int64_t> ends;   // chunk g holds columns [ends[g-1], ends[g]); its event is (*h->up_events)[g]
-};
-
-extern "C" int mla_set_windows(mla_handle h, int width, int64_t min_n, int first_chunk) {
-  if (!h || width < 0 || min_n < 0 || first_chunk < 0) return MLA_E_INVALID;
-  h->win_width = width;
-  h->win_min_n = min_n;
-  h->win_first_chunk = first_chunk;
-  return MLA_OK;
-}
+                    int64_t c1, int b_outer, int64_t deep_block, cudaStream_t s);
 
 extern "C" int mla_set_host_phases(mla_handle h, const int64_t* bounds, int count, int deep) {
   if (!h || count > kMaxHostPhases - 1 || (count > 0 && !bounds)) return MLA_E_INVALID;
@@ -674,13 +611,15 @@ extern "C" int mla_set_host_phases(mla_handle h, const int64_t* bounds, int coun
     if (bounds[i] <= (i ? bounds[i - 1] : 0)) return MLA_E_INVALID;
   h->phase_count = count < 0 ? -1 : count;
   for (int i = 0; i < count; ++i) h->phase_bounds[i] = bounds[i];
-  h->phase_deep = deep ? 1 : 0;
+  h->phase_deep = deep < 0 ? 0 : deep;
   return MLA_OK;
 }
 
 // Window boundaries of the phased entry point: out[0] < out[1] < ... < out[np-1] == n.  Default policy: windows
-// end at n/32, n/16, n/8, n/4 and 3n/8 (whole multiples of b_outer), so the first one waits for 3 % of the
-// upload only and every later one finds its columns uploaded when the window before it is done.
+// end at n/32, n/8 and 3n/8 (whole multiples of b_outer), so the first one waits for 3 % of the upload only and
+// every later one finds its columns uploaded when the window before it is done (measured at n = 32768, 52 GB/s:
+// the third window ends 226 ms after the start, the upload 163 ms; more or later cuts only add panel-bound
+// tall-and-skinny windows, tools/dev_host_phases.py).
 static int host_phase_bounds(mla_handle h, int64_t n, int b_outer, int64_t* out) {
   int np = 0;
   if (h->phase_count > 0) {
@@ -689,8 +628,8 @@ static int host_phase_bounds(mla_handle h, int64_t n, int b_outer, int64_t* out)
       if (c > (np ? out[np - 1] : 0) && c < n) out[np++] = c;
     }
   } else if (h->phase_count < 0 && n >= 8192) {
-    const int64_t num[5] = {1, 2, 4, 8, 12};
-    for (int i = 0; i < 5; ++i) {
+    const int64_t num[3] = {1, 4, 12};
+    for (int i = 0; i < 3; ++i) {
       int64_t c = (n * num[i] / 32) / b_outer * b_outer;
       if (c > (np ? out[np - 1] : 0) && c < n) out[np++] = c;
     }
@@ -731,31 +670,7 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
   cudaStream_t s = h->s_main;
   *((volatile int*)h->progress_host) = 0;
   int64_t bounds[kMaxHostPhases];
-  const bool windowed = use_windows(h, n, b_outer);
-  const int np = windowed ? 0 : host_phase_bounds(h, n, b_outer, bounds);
-  if (windowed) {
-    // two-level factorization behind the upload (getrf_windowed): window-sized chunks, the first window cut once more
-    UploadCtx up;
-    const int64_t W = window_width(h, b_outer);
-    const int64_t fc = (int64_t)h->win_first_chunk / b_outer * b_outer;
-    if (fc > 0 && fc < W) up.ends.push_back(fc);
-    for (int64_t c = W; c < n; c += W) up.ends.push_back(c);
-    up.ends.push_back(n);
-    while (h->up_events->size() < up.ends.size()) {
-      cudaEvent_t e;
-      CK(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      h->up_events->push_back(e);
-    }
-    for (size_t g = 0; g < up.ends.size(); ++g) {
-      const int64_t c0 = g ? up.ends[g - 1] : 0, c1 = up.ends[g];
-      CK(h, cudaMemcpy2DAsync(h->a_dev + c0 * ld, ld * sizeof(double), A_host + c0 * ld_host, ld_host * sizeof(double),
-                              m * sizeof(double), c1 - c0, cudaMemcpyHostToDevice, h->s_up));
-      CK(h, cudaEventRecord((*h->up_events)[g], h->s_up));
-    }
-    LuParams p{h->a_dev, m, n, ld, h->ipiv_dev, b_outer, b_inner, variant, sm_pf, q_chunks, h->info_dev, nullptr, 0};
-    int rc = getrf_windowed(h, p, &up, s);
-    if (rc != MLA_OK) return rc;
-  }
+  const int np = host_phase_bounds(h, n, b_outer, bounds);
   for (int g = 0; g < np; ++g) {
     const int64_t c0 = g ? bounds[g - 1] : 0, c1 = bounds[g];
     CK(h, cudaMemcpy2DAsync(h->a_dev + c0 * ld, ld * sizeof(double), A_host + c0 * ld_host, ld_host * sizeof(double),
@@ -766,7 +681,7 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
   // end, printed to stderr after the call
   const bool timeline = getenv("MLA_HOST_TIMELINE") != nullptr;
   cudaEvent_t tl[3 * kMaxHostPhases + 1];
-  if (timeline && np > 0) {
+  if (timeline) {
     for (int i = 0; i < 3 * np + 1; ++i) cudaEventCreate(&tl[i]);
     cudaEventRecord(tl[3 * np], s);
   }
@@ -775,7 +690,7 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
     CK(h, cudaStreamWaitEvent(s, h->ev_up[g], 0));
     if (timeline) cudaEventRecord(tl[3 * g], s);
     int rc = MLA_OK;
-    if (c0 > 0) rc = catch_up(h, h->a_dev, m, ld, h->ipiv_dev, c0, c0, c1, b_outer, h->phase_deep != 0, s);
+    if (c0 > 0) rc = catch_up(h, h->a_dev, m, ld, h->ipiv_dev, c0, c0, c1, b_outer, h->phase_deep, s);
     if (rc != MLA_OK) return rc;
     if (timeline) cudaEventRecord(tl[3 * g + 1], s);
     h->next_progress = (g == np - 1) ? h->progress_dev : nullptr;
@@ -808,7 +723,7 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
   CK(h, cudaStreamSynchronize(h->s_copy));
   int rc = check_abort(h, s);
   if (info_host) *info_host = *h->info_host;
-  if (timeline && np > 0) {
+  if (timeline) {
     for (int g = 0; g < np; ++g) {
       float t0 = 0, t1 = 0, t2 = 0;
       cudaEventElapsedTime(&t0, tl[3 * np], tl[3 * g]);
@@ -993,216 +908,40 @@ extern "C" int mla_apply_panel(mla_handle h, const double* P, int64_t rows, int6
 // global pivots in ipiv).  All k interchanges first (the L rows are already in their final order, so the new
 // columns must be brought into it before any row of L meets them), then per b_outer-column block [p0, p0 + w)
 // the solve with its unit-lower diagonal block and the rank-w update of the rows below -- one k_apply_panel
-// launch each, without interchanges.  deep: those updates stop at row k and the rows below get ONE multiply of
-// depth k instead (C is then read and written once per window, not once per block).
+// launch each, without interchanges.
+// deep_block > 0: the factored columns are taken in super-blocks of deep_block columns; inside a super-block the
+// rank-w updates stop at the super-block's last row, and the rows below it get ONE multiply of depth deep_block
+// per super-block (C is then read and written once per super-block instead of once per b_outer block, and most
+// of the work runs as a few long multiplies at 34-35 TFLOP/s instead of many short launches that each start with
+// a latency-bound solve).  Same result up to rounding; no longer bit-identical to an unwindowed run.
 static int catch_up(mla_handle h, double* A, int64_t m, int64_t ld, const int32_t* ipiv, int64_t k, int64_t c0,
-                    int64_t c1, int b_outer, bool deep, cudaStream_t s) {
+                    int64_t c1, int b_outer, int64_t deep_block, cudaStream_t s) {
   if (k <= 0 || c1 <= c0) return MLA_OK;
   int rc = laswp_impl(h, A + c0 * ld, m, c1 - c0, ld, ipiv, k, 0, (void*)s, false);
   if (rc != MLA_OK) return rc;
   CK(h, cudaFuncSetAttribute(k_apply_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
   const int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
-  for (int64_t p0 = 0; p0 < k; p0 += b_outer) {
-    const int64_t w = k - p0 < b_outer ? k - p0 : b_outer;
-    const double* P = A + p0 * ld + p0;
-    const int64_t rows = m - p0;
-    if (trsm_use_inverse((int)w)) { rc = launch_diag_inv(h, P, w, ld, h->dinv, s); if (rc != MLA_OK) return rc; }
-    CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
-    CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_DONE, 0, sizeof(unsigned), s));
-    ++h->apply_tag;
-    ApplyArgs a{P, ld, (int)rows, (int)w, A + c0 * ld + p0, ld, (int)(c1 - c0), 0, nullptr, 0, 0, h->plan, h->ctrl,
-                h->lu_state->rprep_done, h->apply_tag, h->dinv, 1, (int)(deep ? k - p0 : rows)};
-    void* args[] = {&a};
-    CK(h, cudaLaunchCooperativeKernel((void*)k_apply_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
-  }
-  if (deep && m > k)
-    return mla_gemm(h, A + c0 * ld + k, m - k, c1 - c0, ld, A + k, ld, A + c0 * ld, ld, k, 1.0, -1.0, nullptr, 0, (void*)s);
-  return MLA_OK;
-}
-
-// ---- windowed (two-level) factorization ----------------------------------------------------------------
-// The columns are cut into windows of W columns.  A window is factored by the persistent kernel restricted to it
-// (getrf_launch with k0: lu_la's own look-ahead / WS / ET schedule inside the window, panels clamped to it) and is
-// then applied to the columns on its right in three steps:
-//   rows   its interchanges, and per b_outer block the solve with the block's unit-lower triangle and the rank-b
-//          update of the rows down to the window's end                      (k_apply_panel without interchanges)
-//   deep   ONE multiply of depth W for all rows below the window            (filler queue, mla_filler.cuh)
-// The deep multiply runs at 34-35 TFLOP/s (C is read and written once per window instead of once per panel), and
-// most of it is off the critical path: the part for the NEXT window's columns is done at once (k_filler, all
-// SMs), the rest rides along as the filler queue of the next window's persistent kernel, whose update-team CTAs
-// execute units of it whenever they would otherwise wait for the panel; what is left is drained afterwards.
-// Every entry of the matrix sees the same operations in the same order whatever the timing: deterministic.
-//
-// With an upload in flight (up != nullptr, mla_getrf_la_host) the same operations are scheduled around the
-// arrival of the column chunks: a window is applied to the columns that are on the device; a chunk that arrives
-// later first receives every window it has missed (left-looking catch-up), in the same order.
-__global__ void k_filler_setup(FillerQ* q, FillerQ v) { *q = v; }
-
-__global__ void __launch_bounds__(kThreads, 1) k_filler(FillerQ* q, unsigned* ctrl) {
-  extern __shared__ __align__(16) double smem[];
-  filler_run(q, nullptr, 0u, ctrl + CW_ABORT, smem);
-}
-
-// queue of  C (m x n) -= A (m x k) @ B (k x n)
-static int filler_setup(mla_handle h, double* C, int64_t m, int64_t n, int64_t ldc, const double* A, int64_t lda,
-                        const double* B, int64_t ldb, int64_t k, cudaStream_t s) {
-  FillerQ v{};
-  v.C = C; v.ldc = ldc; v.A = A; v.lda = lda; v.B = B; v.ldb = ldb;
-  v.m = (int)m; v.n = (int)n; v.k = (int)k; v.kc = kFillerChunk;
-  v.tm_count = (int)((m + GemmUpdateCfg::BM - 1) / GemmUpdateCfg::BM);
-  v.tn_count = (int)((n + GemmUpdateCfg::BN - 1) / GemmUpdateCfg::BN);
-  v.ntiles = v.tm_count * v.tn_count;
-  v.nchunks = (int)((k + v.kc - 1) / v.kc);
-  v.total = v.ntiles * v.nchunks;
-  v.rbt = kRowBlockTiles * 512 / v.kc;
-  if (v.rbt < 4) v.rbt = 4;
-  if (v.rbt > kRowBlockTiles) v.rbt = kRowBlockTiles;
-  if ((size_t)v.ntiles > h->fill_prog_n) return MLA_E_INVALID;   // sized by getrf_windowed for the whole matrix
-  v.prog = h->fill_prog;
-  if (v.ntiles > 0) CK(h, cudaMemsetAsync(h->fill_prog, 0, (size_t)v.ntiles * sizeof(unsigned), s));
-  k_filler_setup<<<1, 1, 0, s>>>(h->fill_dev, v);
-  CK(h, cudaGetLastError());
-  return MLA_OK;
-}
-
-static int filler_drain(mla_handle h, cudaStream_t s) {
-  CK(h, cudaFuncSetAttribute(k_filler, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmUpdateCfg::SMEM_BYTES));
-  k_filler<<<h->num_sms, kThreads, GemmUpdateCfg::SMEM_BYTES, s>>>(h->fill_dev, h->ctrl);
-  CK(h, cudaGetLastError());
-  return MLA_OK;
-}
-
-// "rows" step of window [p0, c0) on columns [a, b), a >= c0.  swaps = false: the columns already carry the
-// window's interchanges (late columns of an upload receive ALL interchanges up front, see getrf_windowed).
-static int window_rows(mla_handle h, const LuParams& p, int64_t p0, int64_t c0, int64_t a, int64_t b, bool swaps,
-                       cudaStream_t s) {
-  if (b <= a) return MLA_OK;
-  int rc = swaps ? laswp_impl(h, p.A + a * p.ld, p.m, b - a, p.ld, p.ipiv, c0, 0, (void*)s, false, p0) : MLA_OK;
-  if (rc != MLA_OK) return rc;
-  CK(h, cudaFuncSetAttribute(k_apply_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemBytes));
-  const int grid = h->num_sms < kMaxTeam ? h->num_sms : kMaxTeam;
-  for (int64_t q = p0; q < c0; q += p.b_outer) {
-    const int64_t w = c0 - q < p.b_outer ? c0 - q : p.b_outer;
-    const double* P = p.A + q * p.ld + q;
-    if (trsm_use_inverse((int)w)) { rc = launch_diag_inv(h, P, w, p.ld, h->dinv, s); if (rc != MLA_OK) return rc; }
-    CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
-    CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_DONE, 0, sizeof(unsigned), s));
-    ++h->apply_tag;
-    ApplyArgs a2{P, p.ld, (int)(p.m - q), (int)w, p.A + a * p.ld + q, p.ld, (int)(b - a), 0, nullptr, 0, 0, h->plan, h->ctrl,
-                 h->lu_state->rprep_done, h->apply_tag, h->dinv, 1, (int)(c0 - q)};
-    void* args[] = {&a2};
-    CK(h, cudaLaunchCooperativeKernel((void*)k_apply_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
-  }
-  return MLA_OK;
-}
-
-// "deep" step of window [p0, c0) on columns [a, b): queue set up; the caller drains it or hands it to a kernel
-static int window_deep_setup(mla_handle h, const LuParams& p, int64_t p0, int64_t c0, int64_t a, int64_t b, cudaStream_t s) {
-  return filler_setup(h, p.A + a * p.ld + c0, p.m - c0, b - a, p.ld, p.A + p0 * p.ld + c0, p.ld, p.A + a * p.ld + p0, p.ld,
-                      c0 - p0, s);
-}
-
-static int getrf_windowed(mla_handle h, const LuParams& p, UploadCtx* up, cudaStream_t s) {
-  if (!h || p.m < p.n || p.n <= 0 || p.ld < p.m) return MLA_E_INVALID;
-  if (p.b_inner < 1 || p.b_outer < p.b_inner || p.b_outer > kMaxPiv) return MLA_E_INVALID;
-  const int64_t W = window_width(h, p.b_outer);
-  const int64_t n = p.n;
-  const int nb = (int)((n + W - 1) / W);
-  auto wend = [&](int j) { return (int64_t)(j + 1) * W < n ? (int64_t)(j + 1) * W : n; };   // window j = [j W, wend(j))
-  {
-    const size_t need = (size_t)((p.m + 127) / 128) * (size_t)((n + 127) / 128);
-    if (h->fill_prog_n < need) {
-      cudaFree(h->fill_prog); h->fill_prog = nullptr; h->fill_prog_n = 0;
-      CK(h, cudaMalloc(&h->fill_prog, need * sizeof(unsigned)));
-      h->fill_prog_n = need;
+  const int64_t sb = deep_block > 0 ? (deep_block + b_outer - 1) / b_outer * b_outer : k;
+  for (int64_t s0 = 0; s0 < k; s0 += sb) {
+    const int64_t s1 = s0 + sb < k ? s0 + sb : k;            // super-block [s0, s1)
+    const bool deep = deep_block > 0 && m > s1;
+    for (int64_t p0 = s0; p0 < s1; p0 += b_outer) {
+      const int64_t w = s1 - p0 < b_outer ? s1 - p0 : b_outer;
+      const double* P = A + p0 * ld + p0;
+      const int64_t rows = m - p0;
+      if (trsm_use_inverse((int)w)) { rc = launch_diag_inv(h, P, w, ld, h->dinv, s); if (rc != MLA_OK) return rc; }
+      CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_NEXT, 0, sizeof(unsigned), s));
+      CK(h, cudaMemsetAsync(h->ctrl + CW_QUEUE_DONE, 0, sizeof(unsigned), s));
+      ++h->apply_tag;
+      ApplyArgs a{P, ld, (int)rows, (int)w, A + c0 * ld + p0, ld, (int)(c1 - c0), 0, nullptr, 0, 0, h->plan, h->ctrl,
+                  h->lu_state->rprep_done, h->apply_tag, h->dinv, 1, (int)(deep ? s1 - p0 : rows)};
+      void* args[] = {&a};
+      CK(h, cudaLaunchCooperativeKernel((void*)k_apply_panel, dim3(grid), dim3(kThreads), args, kDynSmemBytes, s));
     }
-  }
-  // rows the next launch may report as final while it is not the last window: its first row once EVERY column
-  // is on the device and up to date, nothing before that
-  int64_t progress_rows = 0;
-  auto launch = [&](int64_t k0, int64_t n_end, FillerQ* fill, int64_t skip0 = 0, int64_t skip1 = 0) {
-    h->next_progress = up ? h->progress_dev : nullptr;
-    int rc = getrf_launch(h, p.A, p.m, n_end, p.ld, p.ipiv, p.b_outer, p.b_inner, p.variant, p.sm_pf, p.q_chunks, p.info_dev,
-                          p.widths, p.widths_cap, k0, (void*)s, fill, n_end < n ? progress_rows : (1ll << 30), skip0, skip1);
-    h->next_progress = nullptr;
-    return rc;
-  };
-  // chunk bookkeeping of the upload: chunk index whose end is >= col
-  size_t chunks_seen = 0;                 // chunks the factor stream already waits for
-  auto wait_cols = [&](int64_t col_end) -> int {   // make stream s wait until columns [0, col_end) are on the device
-    if (!up) return MLA_OK;
-    while (chunks_seen < up->ends.size() && (chunks_seen == 0 || up->ends[chunks_seen - 1] < col_end)) {
-      CK(h, cudaStreamWaitEvent(s, (*h->up_events)[chunks_seen], 0));
-      ++chunks_seen;
-    }
-    return MLA_OK;
-  };
-  auto arrived_cols = [&]() -> int64_t {           // columns on the device right now (host view)
-    if (!up) return n;
-    size_t g = chunks_seen;
-    while (g < up->ends.size() && cudaEventQuery((*h->up_events)[g]) == cudaSuccess) ++g;
-    return g == 0 ? 0 : up->ends[g - 1];
-  };
-
-  // ---- window 0 (with an upload: in two left-looking steps, so that it can start behind the first small chunk)
-  int rc = MLA_OK;
-  const int64_t w0 = wend(0);
-  int64_t fc = up ? up->ends[0] : w0;
-  if (fc >= w0) fc = w0;
-  if ((rc = wait_cols(fc)) != MLA_OK) return rc;
-  if ((rc = launch(0, fc, nullptr)) != MLA_OK) return rc;
-  if (fc < w0) {
-    if ((rc = wait_cols(w0)) != MLA_OK) return rc;
-    if ((rc = catch_up(h, p.A, p.m, p.ld, p.ipiv, fc, fc, w0, p.b_outer, false, s)) != MLA_OK) return rc;
-    if ((rc = launch(fc, w0, nullptr)) != MLA_OK) return rc;
-  }
-  int64_t have = w0;         // columns [0, have) are on the device AND have received every window applied so far
-  for (int g = 1; g < nb; ++g) {
-    const int64_t p0 = (int64_t)(g - 1) * W, c0 = (int64_t)g * W, c1 = wend(g);
-    // which columns take part in this stage
-    int64_t avail = n;
-    if (up && have < n) {
-      CK(h, cudaEventRecord(h->ev_stage, s));
-      CK(h, cudaEventSynchronize(h->ev_stage));      // the device would wait for the upload anyway; decide late
-      avail = arrived_cols();
-      if (avail < c1) avail = c1;                    // this window's own columns are waited for on the stream
-      avail = (avail >= n) ? n : avail / W * W;      // whole windows only
-      if (avail < c1) avail = c1;
-      if ((rc = wait_cols(avail)) != MLA_OK) return rc;
-    }
-    if (have < c0) have = c0;
-    // window g-1 -> rows step on the columns to its right that have seen every earlier window
-    if ((rc = window_rows(h, p, p0, c0, c0, have, true, s)) != MLA_OK) return rc;
-    // late columns [have, avail): the rows of L they are about to meet are in the order ALL interchanges so far
-    // (windows 0 .. g-1) have left them in, so the late columns get all of those first; then every window they
-    // have missed, in order, the rows step of window g-1 included
-    if (avail > have) {
-      if ((rc = laswp_impl(h, p.A + have * p.ld, p.m, avail - have, p.ld, p.ipiv, c0, 0, (void*)s, false, 0)) != MLA_OK) return rc;
-      for (int q = 0; q < g - 1; ++q) {
-        if ((rc = window_rows(h, p, (int64_t)q * W, (int64_t)(q + 1) * W, have, avail, false, s)) != MLA_OK) return rc;
-        if ((rc = window_deep_setup(h, p, (int64_t)q * W, (int64_t)(q + 1) * W, have, avail, s)) != MLA_OK) return rc;
-        if ((rc = filler_drain(h, s)) != MLA_OK) return rc;
-      }
-      if ((rc = window_rows(h, p, p0, c0, have, avail, false, s)) != MLA_OK) return rc;
-      have = avail;
-    }
-    progress_rows = have >= n ? c0 : 0;
-    // ... deep step on the next window's own columns, at once
-    if ((rc = window_deep_setup(h, p, p0, c0, c0, c1, s)) != MLA_OK) return rc;
-    if ((rc = filler_drain(h, s)) != MLA_OK) return rc;
-    // ... and on the columns right of it as the filler of the next window's kernel
-    const bool fill = have > c1;
-    static const bool nofill = getenv("MLA_WIN_NOFILL") != nullptr;   // development: the deep step as a kernel of its own
-    if (fill && (rc = window_deep_setup(h, p, p0, c0, c1, have, s)) != MLA_OK) return rc;
-    if (fill && nofill && (rc = filler_drain(h, s)) != MLA_OK) return rc;
-    if (fill && !nofill) {
-      // the filler multiplies with the L columns [p0, c0) of window g-1: they keep their row order (that of the
-      // columns the filler updates) until the queue is drained, and only then receive window g's interchanges
-      if ((rc = launch(c0, c1, h->fill_dev, p0, c0)) != MLA_OK) return rc;
-      if ((rc = filler_drain(h, s)) != MLA_OK) return rc;
-      if ((rc = laswp_impl(h, p.A + p0 * p.ld, p.m, c0 - p0, p.ld, p.ipiv, c1, 0, (void*)s, false, c0)) != MLA_OK) return rc;
-    } else {
-      if ((rc = launch(c0, c1, nullptr)) != MLA_OK) return rc;
+    if (deep) {
+      rc = mla_gemm(h, A + c0 * ld + s1, m - s1, c1 - c0, ld, A + s0 * ld + s1, ld, A + c0 * ld + s0, ld, s1 - s0, 1.0, -1.0,
+                    nullptr, 0, (void*)s);
+      if (rc != MLA_OK) return rc;
     }
   }
   return MLA_OK;

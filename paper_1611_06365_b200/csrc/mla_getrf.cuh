@@ -38,7 +38,6 @@
 #include "mla_laswp.cuh"
 #include "mla_panel.cuh"
 #include "mla_trsm.cuh"
-#include "mla_filler.cuh"
 
 namespace mla {
 
@@ -80,7 +79,7 @@ struct TraceEv {
   int items;                     // queue items executed (panel: columns factored)
   int team;                      // CTAs in the panel team of that iteration
 };
-enum TraceKind { TK_PQ = 1, TK_PANEL = 2, TK_RQ = 3, TK_RQ_MERGED = 4, TK_PANEL_ALL = 5, TK_FILL = 6 };
+enum TraceKind { TK_PQ = 1, TK_PANEL = 2, TK_RQ = 3, TK_RQ_MERGED = 4, TK_PANEL_ALL = 5 };
 constexpr int kTraceEvPerCta = 4 * kTraceCap;
 constexpr int kGetrfSmemBytes = 218 * 1024;   // dynamic shared memory of the persistent kernels
 __host__ __device__ constexpr int mla_traced_smem_doubles() { return kGetrfSmemBytes / 8; }
@@ -105,17 +104,6 @@ struct GetrfArgs {
   // columns left of k0 (LEFT items), and the outcome counters / iteration numbering in LuState carry on from
   // the previous launch (the host does not reset LuState).  k0 == 0: a fresh factorization.
   int k0;
-  // Rows reported through `progress` never exceed this: in a window that is not the last one the rows below
-  // the window's first are final only inside the window (the columns to its right get their U rows later).
-  int progress_cap;
-  // Nullable: filler queue (mla_filler.cuh) -- the previous window's deep update of the columns right of this
-  // window.  Update-team CTAs that have drained their queue execute units of it while the panel is still busy.
-  FillerQ* fill;
-  // Columns [left_skip0, left_skip1) (multiples of LEFT_CW, left_skip1 <= k0; 0, 0 = none) do NOT receive this
-  // launch's interchanges: they are the L columns the filler multiplies with, which must keep the row order of the
-  // columns the filler updates (those get this window's interchanges only later).  The host applies the
-  // interchanges to them once the filler queue is drained.
-  int left_skip0, left_skip1;
 };
 
 // item counts of one iteration, derived identically by every CTA from the descriptor
@@ -129,15 +117,7 @@ struct IterShape {
   int rb0;                           // row tiles of the first row block (<= kRowBlockTiles)
 };
 
-// LEFT item l -> first column and width, with the skipped range cut out of [0, q0)
-__device__ __forceinline__ int left_item_col(const GetrfArgs& a, int l, int q0, int& width) {
-  int c = l * LEFT_CW;
-  if (a.left_skip1 > a.left_skip0 && c >= a.left_skip0) c += a.left_skip1 - a.left_skip0;
-  width = imin(LEFT_CW, q0 - c);
-  return c;
-}
-
-__device__ __forceinline__ IterShape iter_shape(const LuState* st, int m, int n, int grid, int left_skip) {
+__device__ __forceinline__ IterShape iter_shape(const LuState* st, int m, int n, int grid) {
   IterShape s;
   s.q0 = *((volatile const int*)&st->q0);
   s.q1 = *((volatile const int*)&st->q1);
@@ -166,7 +146,7 @@ __device__ __forceinline__ IterShape iter_shape(const LuState* st, int m, int n,
   s.rb0 = imin(kRowBlockTiles, s.tmc);
   s.gs = s.rb0 + 2;
   s.rq_gemm = s.nrs * s.tmc;
-  s.nleft = (s.q0 - left_skip + LEFT_CW - 1) / LEFT_CW;
+  s.nleft = (s.q0 + LEFT_CW - 1) / LEFT_CW;
   s.rq_total = s.nrs * (s.tmc + 2) + imax(0, s.nleft - s.nrs);
   return s;
 }
@@ -431,9 +411,9 @@ __device__ MLA_RQ_ATTR int run_queue(const GetrfArgs& a, const IterShape& s, dou
       const int c0 = s.q1 + s.w + it.strip * TRSM_CW;
       item_prep(a, s, c0, imin(TRSM_CW, a.n - c0), &st->rprep_done[it.strip], smem);
     } else if (it.kind == 4) {
-      int lw;
-      const int c0 = left_item_col(a, it.strip, s.q0, lw);
-      laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, lw, (a.plan + (s.it & 1))->ref(), smem, kLaswpBufDoubles);
+      const int c0 = it.strip * LEFT_CW;
+      laswp_apply_cols(a.A + (int64_t)c0 * a.ld + s.q0, a.ld, imin(LEFT_CW, s.q0 - c0), (a.plan + (s.it & 1))->ref(), smem,
+                       kLaswpBufDoubles);
     }
     if (dbgc2 && it.kind != 0) {
       if (it.kind <= 2) { g_dbg[2] += globaltimer_ns() - dt1; g_dbg[3] += 1; }
@@ -536,7 +516,6 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
       ks.singular = *((volatile const int*)&st->singular); ks.et_events = *((volatile const int*)&st->et_events);
       ks.n_panels = *((volatile const int*)&st->n_panels); ks.ws_joins = *((volatile const int*)&st->ws_joins);
       ks.it_next = *((volatile const int*)&st->it) + 1;
-      ks.b_target = *((volatile const int*)&st->b_target);   // the width schedule carries on across windows
       if constexpr (TRACE) {
         // the CTA's event ring carries on behind the records of the earlier windows
         int used = 0;
@@ -583,7 +562,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
   // (a later window's first panel is factored by the panel team instead, like the look-ahead panel it would
   // have been in an unwindowed run: the factors then do not depend on where the windows are cut)
   {
-    const int w0 = imin(ks.b_target, n - k0);
+    const int w0 = imin(a.b_outer, n - k0);
     double* const P0 = a.A + (int64_t)k0 * a.ld + k0;
     const int it_first = ks.it_next;
     if (k0 > 0 && la) {
@@ -632,7 +611,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
         if (a.widths && n_panels < a.widths_cap) a.widths[n_panels] = k_new;
         ++n_panels;
         if (k_new < w_sched) { ++et_events; b_target = imax(a.b_inner, k_new); }
-        else if (q1_of_panel > 0) b_target = imin(a.b_outer, 2 * b_target);
+        else if (q1_of_panel > k0) b_target = imin(a.b_outer, 2 * b_target);
         const int pend = q1_of_panel + w_sched;
         const int q0 = q1_of_panel, q1 = q1_of_panel + k_new;
         ks.q0 = q0; ks.q1 = q1; ks.b_target = b_target; ks.n_panels = n_panels; ks.et_events = et_events;
@@ -640,7 +619,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
         if (a.progress) {
           // every write to rows < q0 precedes the grid barrier above; later work touches rows >= q0 only
           __threadfence_system();
-          *((volatile int*)a.progress) = imin(q0, a.progress_cap);
+          *((volatile int*)a.progress) = q0;
         }
         st->w = imin(b_target, n - q1);
         st->b_target = b_target;
@@ -675,7 +654,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
         ks.pf_target = 0u;                                   // the panel team is re-formed every iteration
         if (bid == 0) ks.t_iter0 = globaltimer_ns();
       }
-      sh = iter_shape(st, m, n, G, a.left_skip1 - a.left_skip0);
+      sh = iter_shape(st, m, n, G);
       ks.q1_of_panel = sh.q1;
       ks.w_sched = sh.w;
       ks.b_target = *((volatile const int*)&st->b_target);
@@ -685,9 +664,9 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
     if (*((volatile const int*)&st->done)) {
       // ---- final_sync (lu.py:328-332): last panel's interchanges for the columns to its left ------
       for (int l = bid; l < sh.nleft; l += G) {
-        int lw;
-        const int c0 = left_item_col(a, l, sh.q0, lw);
-        laswp_apply_cols(a.A + (int64_t)c0 * a.ld + sh.q0, a.ld, lw, (a.plan + (sh.it & 1))->ref(), smem, kLaswpBufDoubles);
+        int c0 = l * LEFT_CW;
+        laswp_apply_cols(a.A + (int64_t)c0 * a.ld + sh.q0, a.ld, imin(LEFT_CW, sh.q0 - c0), (a.plan + (sh.it & 1))->ref(), smem,
+                         kLaswpBufDoubles);
       }
       break;
     }
@@ -777,13 +756,6 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
         const int ex = run_queue(a, sh, smem, 1, et);
         if (ex < 0) break;
         tr_end(TK_RQ, sh.it, ex, ks.sm_pf);
-        if (a.fill) {
-          // nothing left in this iteration's queues: units of the filler multiply until the panel is done
-          tr_begin();
-          const int fx = filler_run(a.fill, &st->pf_done, (unsigned)sh.it, abort_word, smem);
-          if (fx < 0) break;
-          if (fx > 0) tr_end(TK_FILL, sh.it, fx, ks.sm_pf);
-        }
       }
     }
   }

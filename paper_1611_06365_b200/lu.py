@@ -25,9 +25,7 @@ class LuResult:
     """Outcome of a factorization; the factors live in the input matrix (reference lu.py:33-41).
     `widths` (extension) lists every panel's factored width in order, which makes an ET run
     replayable on the CPU oracle; `ws_joins` counts iterations in which panel SMs joined the update;
-    `t_pf_peak` is the largest panel team an adaptive split (pool.t_pf_max) used; `window` the window width
-    of the two-level factorization the run used (0: none) -- panels never cross a multiple of it, so the
-    oracle replays the run with clamp=window."""
+    `t_pf_peak` is the largest panel team an adaptive split (pool.t_pf_max) used."""
 
     ipiv: PivotVector
     cols_factored: int
@@ -37,7 +35,6 @@ class LuResult:
     widths: tuple = ()
     ws_joins: int = 0
     t_pf_peak: int = 0
-    window: int = 0
 
 
 def _check_tall(a: torch.Tensor) -> tuple[int, int, int]:
@@ -193,23 +190,19 @@ def lu_la(a: torch.Tensor, policy: Policy, pool: SmPool | None = None, cfg=None)
                                               int(policy.q), ctypes.byref(info), widths, cap,
                                               _stream(a)), pool.handle, "lu_la")
     w = tuple(int(x) for x in widths[:min(cap, int(info.n_panels))])
-    win = pool.window_for(n, b_o)
     return LuResult(PivotVector(dev_piv.cpu().numpy(), device=dev_piv), n, bool(info.singular),
-                    int(info.et_events), et_widths_from(w, n, b_o, b_i, win), w, int(info.ws_joins),
-                    int(info.sm_pf_peak), win)
+                    int(info.et_events), et_widths_from(w, n, b_o, b_i), w, int(info.ws_joins),
+                    int(info.sm_pf_peak))
 
 
-def et_widths_from(widths, n: int, b_o: int, b_i: int, clamp: int = 0) -> tuple:
-    """The cut widths among `widths` (reference et_widths), replaying lu.py:318-323 (clamp > 0: panels never
-    cross a multiple of `clamp` columns -- the windowed factorization's one extra schedule rule)."""
+def et_widths_from(widths, n: int, b_o: int, b_i: int) -> tuple:
+    """The cut widths among `widths` (reference et_widths), replaying lu.py:318-323."""
     out = []
     if not widths:
         return ()
     b_target, q1 = b_o, widths[0]
     for k_new in widths[1:]:
         w = min(b_target, n - q1)
-        if clamp > 0:
-            w = min(w, clamp - q1 % clamp)
         if k_new < w:
             out.append(k_new)
             b_target = max(b_i, k_new)
@@ -219,18 +212,15 @@ def et_widths_from(widths, n: int, b_o: int, b_i: int, clamp: int = 0) -> tuple:
     return tuple(out)
 
 
-def et_schedule_from(widths, n: int, b_o: int, b_i: int, clamp: int = 0) -> list[int]:
+def et_schedule_from(widths, n: int, b_o: int, b_i: int) -> list[int]:
     """Per-iteration 'trip poll' list that makes the CPU oracle replay an ET run: entry it-1 is the
-    number of inner blocks after which iteration it's panel was cut (0 = not cut).  clamp = LuResult.window
-    (pass the same value to the oracle's lu_la)."""
+    number of inner blocks after which iteration it's panel was cut (0 = not cut)."""
     out = []
     if not widths:
         return out
     b_target, q1 = b_o, widths[0]
     for k_new in widths[1:]:
         w = min(b_target, n - q1)
-        if clamp > 0:
-            w = min(w, clamp - q1 % clamp)
         if k_new < w:
             out.append(k_new // b_i)
             b_target = max(b_i, k_new)

@@ -32,26 +32,6 @@ class SmPool:
         self._t_pf_max = None
         self._closed = False
         self.t_pf_max = 0 if t_pf_max is None else t_pf_max
-        # windowed (two-level) factorization, mla_set_windows: window width in columns (0 = off), smallest n it
-        # is used for, and the first upload chunk of the host entry point
-        self.window, self.window_min_n, self.window_first_chunk = 4096, 16384, 1024
-
-    def set_windows(self, width: int, min_n: int | None = None, first_chunk: int | None = None) -> None:
-        """Window width of the two-level factorization (0 switches it off: one persistent launch)."""
-        min_n = self.window_min_n if min_n is None else int(min_n)
-        first_chunk = self.window_first_chunk if first_chunk is None else int(first_chunk)
-        if int(width) < 0 or min_n < 0 or first_chunk < 0:
-            raise ValueError("window width, min_n and first_chunk must be >= 0")
-        _capi.check(_capi.lib().mla_set_windows(self.handle, int(width), min_n, first_chunk), self._h, "mla_set_windows")
-        self.window, self.window_min_n, self.window_first_chunk = int(width), min_n, first_chunk
-
-    def window_for(self, n: int, b_outer: int) -> int:
-        """The window width a factorization of n columns with outer block b_outer runs with (0: not windowed).
-        Panels never cross a multiple of it, which is what the CPU oracle's `clamp` replays."""
-        w = self.window // b_outer * b_outer if b_outer <= self.window else 0
-        while w > 0 and w % 256:          # also a whole multiple of the kernel's LEFT item width
-            w -= b_outer
-        return w if (w > 0 and n >= self.window_min_n and n > w) else 0
 
     @property
     def t_pf_max(self) -> int:

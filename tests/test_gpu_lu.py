@@ -174,6 +174,83 @@ def test_host_entry_streams_out_the_same_factors(mla, m, n, pinned):
         assert info.n_panels == len(r.widths)
 
 
+def _set_host_phases(pool, bounds, deep):
+    import ctypes
+    from paper_1611_06365_b200 import _capi
+    if bounds is None:
+        rc = _capi.lib().mla_set_host_phases(pool.handle, None, -1, deep)
+    else:
+        arr = (ctypes.c_int64 * max(1, len(bounds)))(*bounds)
+        rc = _capi.lib().mla_set_host_phases(pool.handle, arr, len(bounds), deep)
+    _capi.check(rc, pool.handle, "mla_set_host_phases")
+
+
+@pytest.mark.parametrize("m,n,b_o,b_i,bounds", [(3000, 3000, 256, 32, [256, 768, 1536]), (5000, 3500, 256, 32, [1024, 2048]),
+                                                (4096, 4096, 128, 32, [128, 256, 384, 512, 4000]), (2500, 2500, 256, 32, [700, 1900])])
+def test_host_entry_factors_behind_the_upload(mla, m, n, b_o, b_i, bounds):
+    """mla_getrf_la_host with column windows (mla_set_host_phases): chunked upload, left-looking catch-up of each
+    window, persistent kernel restricted to the window.  Per-block catch-up (deep = 0): every entry sees the
+    operations of an unwindowed run in the same order, so the variants without ET must reproduce the device
+    path BIT FOR BIT wherever the windows are cut; with deep multiplies (deep > 0) and for lu_et: identical
+    pivots and factors within the 1e-10 parity bound."""
+    import ctypes
+    import torch
+    from paper_1611_06365_b200 import _capi
+    pool = mla.default_pool()
+    a = gen(m, n, 23)
+    pristine = torch.from_numpy(np.array(a.T, order="C", copy=True))
+    try:
+        for variant in ("lu_mb", "lu", "lu_et"):
+            d = mla.from_numpy(a)
+            r = mla.lu_la(d, mla.Policy(variant, mla.BlockConfig(b_o, b_i)), pool)
+            want = mla.to_numpy(d)
+            scale = np.maximum(np.abs(want), np.abs(want).max(axis=0, keepdims=True))
+            for deep in (0, 512, 1 << 20):
+                _set_host_phases(pool, bounds, deep)
+                host = pristine.clone().pin_memory()
+                ipiv = torch.empty(n, dtype=torch.int32)
+                info = _capi.LuInfo()
+                rc = _capi.lib().mla_getrf_la_host(pool.handle, host.data_ptr(), m, n, m, ipiv.data_ptr(), b_o, b_i,
+                                                   _capi.VARIANT_CODES[variant], pool.t_pf, 1, ctypes.byref(info))
+                _capi.check(rc, pool.handle, "mla_getrf_la_host")
+                got = host.numpy().T
+                assert np.array_equal(ipiv.numpy().astype(np.int64), r.ipiv.ipiv), (variant, deep)
+                assert float((np.abs(got - want) / scale).max()) <= 1e-10, (variant, deep)
+                if variant != "lu_et" and deep == 0:
+                    assert np.array_equal(got, want), (variant, "windowed host entry differs from the device path")
+                    assert info.n_panels == len(r.widths)
+    finally:
+        _set_host_phases(pool, None, 4096)
+
+
+def test_host_entry_default_windows_at_config2_size(mla):
+    """The default window policy (n/32, n/8, 3n/8; deep catch-up) is active from n = 8192: config 2's matrix
+    through the host entry point against the reference-pinned golden pivots and the device path's factors."""
+    import ctypes
+    import torch
+    from paper_1611_06365_b200 import _capi
+    n, b_o, b_i = 8192, 256, 32
+    pool = mla.default_pool()
+    a = mla.make_config_matrix("config2")
+    g = np.load(os.path.join(GOLDEN_DIR, "golden_config2.npz"))
+    d = mla.from_numpy(a)
+    r = mla.lu_la(d, mla.Policy("lu_mb", mla.BlockConfig(b_o, b_i)), pool)
+    want = mla.to_numpy(d)
+    host = torch.from_numpy(np.array(a.T, order="C", copy=True)).pin_memory()
+    ipiv = torch.empty(n, dtype=torch.int32).pin_memory()
+    info = _capi.LuInfo()
+    rc = _capi.lib().mla_getrf_la_host(pool.handle, host.data_ptr(), n, n, n, ipiv.data_ptr(), b_o, b_i,
+                                       _capi.VARIANT_CODES["lu_et"], pool.t_pf, 1, ctypes.byref(info))
+    _capi.check(rc, pool.handle, "mla_getrf_la_host")
+    got = host.numpy().T
+    assert np.array_equal(ipiv.numpy().astype(np.int64), g["ipiv"].astype(np.int64))
+    assert np.array_equal(r.ipiv.ipiv, g["ipiv"].astype(np.int64))
+    scale = np.maximum(np.abs(want), np.abs(want).max(axis=0, keepdims=True))
+    assert float((np.abs(got - want) / scale).max()) <= 1e-10
+    berr = oracle.residual_lu(a, got, ipiv.numpy().astype(np.int64)) / (n * np.finfo(np.float64).eps)
+    assert berr <= 10.0, berr
+
+
 def test_tall_singular_empty_dominant(mla):  # test_lu.py:94-106, 226-244
     run_and_check(mla, gen(300, 200, 3), 64, 16, "lu_et", what="tall 300x200")
     run_and_check(mla, gen(900, 333, 3), 128, 32, "lu_mb", what="tall 900x333")

@@ -40,7 +40,7 @@ def check():
             r = mla.lu_la(d, mla.Policy(variant, mla.BlockConfig(b_o, b_i)), pool)
             want = mla.to_numpy(d)
             pristine = torch.from_numpy(np.array(a.T, order="C", copy=True))
-            for deep in (0, 1):
+            for deep in (0, 512, 100000):
                 set_phases(bounds, deep)
                 host = pristine.clone().pin_memory()
                 ipiv, info, _ = host_call(host, m, n, b_o, b_i, variant)
@@ -67,9 +67,10 @@ def timing(n):
     del a
     work = torch.empty_like(host_t).pin_memory()
     f = n // 32
-    layouts = [("one phase", [], 0), ("n/32 n/8 3n/8", [f, 4 * f, 12 * f], 0), ("n/32 n/8 3n/8 deep", [f, 4 * f, 12 * f], 1),
-               ("n/32 n/8 n/4 deep", [f, 4 * f, 8 * f], 1), ("n/32 3n/32 n/4 deep", [f, 3 * f, 8 * f], 1),
-               ("n/32 n/8 n/2 deep", [f, 4 * f, 16 * f], 1)]
+    layouts = [("one phase", [], 0), ("default bounds, per panel", None, 0), ("default, deep 2048", None, 2048),
+               ("default, deep 4096", None, 4096), ("default, deep 1024", None, 1024), ("default, deep whole", None, 1 << 20),
+               ("n/32 n/8 5n/16 deep 2048", [f, 4 * f, 10 * f], 2048), ("3n/64 5n/32 13n/32 deep 2048", [3 * f // 2, 5 * f, 13 * f], 2048),
+               ("n/32 n/8 n/4 3n/8 deep 2048", [f, 4 * f, 8 * f, 12 * f], 2048)]
     for variant in VARIANTS:
         for name, bounds, deep in layouts:
             set_phases(bounds, deep)
