@@ -425,7 +425,8 @@ def run_ours(args):
         e2e = {"value": round(flops / e / 1e9, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n * n,
                "d2h_bytes_per_step": 8 * n * n + 4 * n, "ms_per_step": round(e * 1e3, 2), "timed_calls": len(e_times),
                "ms_min_max": [round(min(e_times) * 1e3, 2), round(max(e_times) * 1e3, 2)],
-               "api": "mla_getrf_la_host (C ABI, pinned host buffers)"}
+               "api": "mla_getrf_la_host (C ABI, pinned host buffers; chunked upload, windows n/32 n/8 3n/8 factored "
+                      "behind it, finished rows streamed out under the last window)"}
 
     cpu = None if args.no_cpu else cpu_baseline(cfg, b_o, b_i)
     out = {

@@ -67,10 +67,9 @@ def timing(n):
     del a
     work = torch.empty_like(host_t).pin_memory()
     f = n // 32
-    layouts = [("one phase", [], 0), ("default bounds, per panel", None, 0), ("default, deep 2048", None, 2048),
-               ("default, deep 4096", None, 4096), ("default, deep 1024", None, 1024), ("default, deep whole", None, 1 << 20),
-               ("n/32 n/8 5n/16 deep 2048", [f, 4 * f, 10 * f], 2048), ("3n/64 5n/32 13n/32 deep 2048", [3 * f // 2, 5 * f, 13 * f], 2048),
-               ("n/32 n/8 n/4 3n/8 deep 2048", [f, 4 * f, 8 * f, 12 * f], 2048)]
+    layouts = [("one phase", [], 0), ("default", None, 4096)]
+    for spec in os.environ.get("LAYOUTS", "1,4,12,22;1,4,12,20;1,4,12,18,25;1,4,10,20;1,4,12,17,22,27").split(";"):
+        layouts.append((f"{spec} /32", [int(x) * f for x in spec.split(",")], 4096))
     for variant in VARIANTS:
         for name, bounds, deep in layouts:
             set_phases(bounds, deep)
