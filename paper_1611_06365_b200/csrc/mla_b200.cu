@@ -660,9 +660,10 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
   //  * Upload || factor: the columns travel in chunks on their own stream, and the factorization runs window by
   //    window behind them (left-looking between windows): window [c0, c1) waits for its chunk only, is brought
   //    up to date with the columns [0, c0) factored so far (catch_up: every interchange, then per 512-column
-  //    block a solve and a rank-512 update -- the operations an unwindowed run applies to these columns, in the
-  //    same order per entry, so the factors are the same bit for bit) and is then factored by the persistent
-  //    kernel restricted to it (look-ahead, WS and ET inside the window).  The last window takes everything left.
+  //    block a solve and a rank-512 update -- with deep == 0 exactly the operations an unwindowed run applies to
+  //    these columns, in the same order per entry, so the factors are the same bit for bit; by default most of
+  //    the update runs as multiplies of depth 4096) and is then factored by the persistent kernel restricted to
+  //    it (look-ahead, WS and ET inside the window).  The last window takes everything left.
   //  * Factor || download: once an outer iteration of the LAST window has started with its panel at row q0,
   //    rows [0, q0) of the whole matrix are final (later interchanges, solves and updates only touch rows
   //    >= q0), so they are copied to the host as row blocks on a second stream.  The kernel reports q0 through
@@ -671,12 +672,16 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
   *((volatile int*)h->progress_host) = 0;
   int64_t bounds[kMaxHostPhases];
   const int np = host_phase_bounds(h, n, b_outer, bounds);
-  for (int g = 0; g < np; ++g) {
+  // (a chunk's copy is issued right in front of its window's work, not all copies first: from pageable host
+  // memory a copy blocks the calling thread while it is staged, and the windows before it should already be
+  // running on the device by then)
+  auto upload_chunk = [&](int g) -> int {
     const int64_t c0 = g ? bounds[g - 1] : 0, c1 = bounds[g];
     CK(h, cudaMemcpy2DAsync(h->a_dev + c0 * ld, ld * sizeof(double), A_host + c0 * ld_host, ld_host * sizeof(double),
                             m * sizeof(double), c1 - c0, cudaMemcpyHostToDevice, h->s_up));
     CK(h, cudaEventRecord(h->ev_up[g], h->s_up));
-  }
+    return MLA_OK;
+  };
   // MLA_HOST_TIMELINE=1 (development): device stamps at every window's catch-up start / kernel start / kernel
   // end, printed to stderr after the call
   const bool timeline = getenv("MLA_HOST_TIMELINE") != nullptr;
@@ -687,9 +692,10 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
   }
   for (int g = 0; g < np; ++g) {
     const int64_t c0 = g ? bounds[g - 1] : 0, c1 = bounds[g];
+    int rc = upload_chunk(g);
+    if (rc != MLA_OK) return rc;
     CK(h, cudaStreamWaitEvent(s, h->ev_up[g], 0));
     if (timeline) cudaEventRecord(tl[3 * g], s);
-    int rc = MLA_OK;
     if (c0 > 0) rc = catch_up(h, h->a_dev, m, ld, h->ipiv_dev, c0, c0, c1, b_outer, h->phase_deep, s);
     if (rc != MLA_OK) return rc;
     if (timeline) cudaEventRecord(tl[3 * g + 1], s);

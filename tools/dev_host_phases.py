@@ -61,6 +61,7 @@ def check():
 
 def timing(n):
     b_o, b_i = 512, 64
+    pool.t_pf_max = int(os.environ.get("T_PF_MAX", "0"))       # malleable panel team inside the windows
     a = mla.alloc_matrix(n, n)
     mla.fill_random(a, 3, 2.0, -1.0)
     host_t = a.t().contiguous().cpu().pin_memory()          # (n, n): rows are the matrix's columns

@@ -44,3 +44,25 @@ for k, v in sorted(tot.items(), key=lambda kv: -kv[1][0]):
 txt += ["", "# per-launch k_getrf durations (ms):"] + ["%.2f" % x for x in per]
 open(f"profiles/{R}_launches_bench_n32768.txt", "w").write("\n".join(txt) + "\n")
 print("\n".join(txt))
+
+# launch list of the same command with the e2e leg on (mla_getrf_la_host: one persistent launch per window +
+# the catch-up launches between them), if it was captured
+import os
+if os.path.exists(f"profiles/{R}_launches_bench_e2e.csv"):
+    rows = [r for r in csv.reader(l for l in open(f"profiles/{R}_launches_bench_e2e.csv") if l.startswith('"'))]
+    hdr = rows[0]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    tot = collections.OrderedDict()
+    for r in rows[1:]:
+        name = r[ki].split("(")[0][:70]
+        t = tot.setdefault(name, [0.0, 0])
+        t[0] += float(r[vi]); t[1] += 1
+    total = sum(v[0] for v in tot.values())
+    txt = ["# ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 1 --warmup 3 --no-cpu",
+           "# (value leg: 4 k_getrf launches of the whole matrix; e2e leg: 6 calls of mla_getrf_la_host, each 4 windowed",
+           "#  k_getrf launches + catch-up = k_laswp_* + k_diag_inv + k_apply_panel + k_gemm; serialised, cold cache: SHARES)",
+           "# total device time %.1f ms over %d launches" % (total / 1e6, sum(v[1] for v in tot.values()))]
+    for k, v in sorted(tot.items(), key=lambda kv: -kv[1][0]):
+        txt.append("%10.2f ms  %5.1f%%  x%-4d %s" % (v[0] / 1e6, 100 * v[0] / total, v[1], k))
+    open(f"profiles/{R}_launches_bench_e2e.txt", "w").write("\n".join(txt) + "\n")
+    print("\n".join(txt))
