@@ -15,6 +15,7 @@ import oracle, cases
 from parity import assert_parity, BACKWARD_TOL
 ncases = int(sys.argv[1]) if len(sys.argv) > 1 else 150
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+HOST = os.environ.get("FUZZ_HOST", "1") != "0"     # also run every case through the windowed host entry point
 pool = mla.SmPool()
 EPS = np.finfo(np.float64).eps
 bad = 0
@@ -45,6 +46,32 @@ for it in range(ncases):
         if not r.singular:
             berr = oracle.residual_lu(a, mla.to_numpy(d), r.ipiv.ipiv) / (max(m, n) * EPS)
             assert berr <= BACKWARD_TOL, f"backward error {berr}"
+        # the host entry point with random windows (mla_set_host_phases): per-block catch-up must reproduce the
+        # device path bit for bit for the variants without ET; deep catch-up / lu_et within the parity bound
+        if HOST and n >= 2 and not r.singular and kind >= 0.15:
+            import ctypes
+            from paper_1611_06365_b200 import _capi
+            ncut = int(rng.integers(1, 5))
+            bounds = sorted(set(int(x) for x in rng.integers(1, n, size=ncut)))
+            deep = int(rng.choice([0, 0, b_o, 4 * b_o, 1 << 20]))
+            arr = (ctypes.c_int64 * len(bounds))(*bounds)
+            _capi.check(_capi.lib().mla_set_host_phases(pool.handle, arr, len(bounds), deep), pool.handle, "phases")
+            host = torch.from_numpy(np.array(a.T, order="C", copy=True))
+            if rng.random() < 0.5:
+                host = host.pin_memory()
+            ipiv = torch.empty(n, dtype=torch.int32)
+            info = _capi.LuInfo()
+            t_use = min(max(t_pf, 1), pool.t - 1)
+            rc = _capi.lib().mla_getrf_la_host(pool.handle, host.data_ptr(), m, n, m, ipiv.data_ptr(), b_o, b_i,
+                                               _capi.VARIANT_CODES[variant], t_use, 1, ctypes.byref(info))
+            _capi.check(rc, pool.handle, "mla_getrf_la_host")
+            got, want = host.numpy().T, mla.to_numpy(d)
+            assert np.array_equal(ipiv.numpy().astype(np.int64), r.ipiv.ipiv), f"host entry pivots (bounds {bounds}, deep {deep})"
+            scale = np.maximum(np.abs(want), np.abs(want).max(axis=0, keepdims=True))
+            scale[scale == 0] = 1.0
+            assert float((np.abs(got - want) / scale).max()) <= 1e-10, f"host entry factors (bounds {bounds}, deep {deep})"
+            if variant != "lu_et" and deep == 0 and pool.t_pf_max == 0:
+                assert np.array_equal(got, want), f"host entry not bitwise (bounds {bounds})"
     except Exception as e:                # keep going, report everything
         bad += 1
         print(f"FAIL case {it}: m={m} n={n} b={b_o}/{b_i} {variant} t_pf={t_pf} max={pool.t_pf_max} kind={kind:.2f}: {type(e).__name__} {str(e)[:200]}", flush=True)
