@@ -672,9 +672,17 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
   *((volatile int*)h->progress_host) = 0;
   int64_t bounds[kMaxHostPhases];
   const int np = host_phase_bounds(h, n, b_outer, bounds);
-  // (a chunk's copy is issued right in front of its window's work, not all copies first: from pageable host
-  // memory a copy blocks the calling thread while it is staged, and the windows before it should already be
-  // running on the device by then)
+  // Pinned host memory: all chunk copies are queued at once (they run back to back on the copy engine whatever
+  // the calling thread does afterwards).  Pageable host memory: a copy blocks the calling thread while it is
+  // staged, so each chunk's copy is issued right in front of its window's work -- the windows before it are then
+  // already running on the device.
+  bool pinned = false;
+  {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, A_host) == cudaSuccess) pinned = (pa.type == cudaMemoryTypeHost);
+    else cudaGetLastError();
+    if (getenv("MLA_UPLOAD_INTERLEAVED")) pinned = false;   // development: force the pageable order
+  }
   auto upload_chunk = [&](int g) -> int {
     const int64_t c0 = g ? bounds[g - 1] : 0, c1 = bounds[g];
     CK(h, cudaMemcpy2DAsync(h->a_dev + c0 * ld, ld * sizeof(double), A_host + c0 * ld_host, ld_host * sizeof(double),
@@ -692,7 +700,9 @@ extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_
   }
   for (int g = 0; g < np; ++g) {
     const int64_t c0 = g ? bounds[g - 1] : 0, c1 = bounds[g];
-    int rc = upload_chunk(g);
+    int rc = MLA_OK;
+    if (!pinned) rc = upload_chunk(g);
+    else if (g == 0) for (int u = 0; u < np && rc == MLA_OK; ++u) rc = upload_chunk(u);
     if (rc != MLA_OK) return rc;
     CK(h, cudaStreamWaitEvent(s, h->ev_up[g], 0));
     if (timeline) cudaEventRecord(tl[3 * g], s);
