@@ -70,7 +70,7 @@ def timing(n):
     f = n // 32
     layouts = [("one phase", [], 0), ("default", None, 4096)]
     for spec in os.environ.get("LAYOUTS", "1,4,12,22;1,4,12,20;1,4,12,18,25;1,4,10,20;1,4,12,17,22,27").split(";"):
-        layouts.append((f"{spec} /32", [int(x) * f for x in spec.split(",")], 4096))
+        layouts.append((f"{spec} /32", [int(float(x) * f) for x in spec.split(",")], 4096))
     for variant in VARIANTS:
         for name, bounds, deep in layouts:
             set_phases(bounds, deep)

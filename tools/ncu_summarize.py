@@ -21,7 +21,8 @@ FILES = [("getrf_n16384", "k_getrf, n=16384 b=512/64 lu_et sm_pf 32 (same code p
          ("gemm_16384_k256", "k_gemm, 16384 x 16384 x 256"),
          ("laswp_trsm", "k_laswp_apply / k_trsm (tools/dev_ops_time.py)"),
          ("panel", "k_panel (tools/dev_panel_time2.py)"),
-         ("apply_panel", "k_apply_panel (multi-GPU driver's fused update step; tools/dev_dist_time.py 16384 512 lu_mb)")]
+         ("apply_panel", "k_apply_panel (multi-GPU driver's fused update step; tools/dev_dist_time.py 16384 512 lu_mb)"),
+         ("gemm_deep", "k_gemm, 20480 x 20480 x 4096 -- the deep multiply of the host entry point's catch-up (tools/dev_gemm_one.py)")]
 out = ["# ncu --set full --clock-control none summaries (tools/profile_round.sh, tools/ncu_summarize.py); one block per captured launch"]
 for stem, title in FILES:
     path = f"gpurun_out/{R}_{stem}_raw.csv"
