@@ -638,9 +638,27 @@ static int host_phase_bounds(mla_handle h, int64_t n, int b_outer, int64_t* out)
   return np;
 }
 
+static int getrf_la_host_impl(mla_handle h, double* A_host, int64_t m, int64_t n, int64_t ld_host,
+                              int32_t* ipiv_host, int b_outer, int b_inner, int variant, int sm_pf,
+                              int q_chunks, mla_lu_info* info_host);
+
 extern "C" int mla_getrf_la_host(mla_handle h, double* A_host, int64_t m, int64_t n, int64_t ld_host,
                                  int32_t* ipiv_host, int b_outer, int b_inner, int variant, int sm_pf,
                                  int q_chunks, mla_lu_info* info_host) {
+  int rc = getrf_la_host_impl(h, A_host, m, n, ld_host, ipiv_host, b_outer, b_inner, variant, sm_pf, q_chunks, info_host);
+  if (rc != MLA_OK && h) {
+    // whatever failed: no copy engine or kernel may still touch the caller's buffers after the return
+    cudaStreamSynchronize(h->s_up);
+    cudaStreamSynchronize(h->s_main);
+    cudaStreamSynchronize(h->s_copy);
+    h->next_progress = nullptr;
+  }
+  return rc;
+}
+
+static int getrf_la_host_impl(mla_handle h, double* A_host, int64_t m, int64_t n, int64_t ld_host,
+                              int32_t* ipiv_host, int b_outer, int b_inner, int variant, int sm_pf,
+                              int q_chunks, mla_lu_info* info_host) {
   if (!h || m < n || n < 0 || (m > 0 && ld_host < m)) return MLA_E_INVALID;
   if (b_inner < 1 || b_outer < b_inner || b_outer > kMaxPiv) return MLA_E_INVALID;
   if (n == 0) { if (info_host) memset(info_host, 0, sizeof(*info_host)); return MLA_OK; }

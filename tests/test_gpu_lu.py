@@ -224,6 +224,44 @@ def test_host_entry_factors_behind_the_upload(mla, m, n, b_o, b_i, bounds):
         _set_host_phases(pool, None, 4096)
 
 
+def test_host_entry_rejects_bad_arguments_and_stays_usable(mla):
+    """Argument errors of mla_getrf_la_host come back as MLA_E_INVALID (-1) before or after the chunk copies were
+    queued (a bad variant is only seen by the first window's launch: the entry point then drains its streams),
+    the host matrix is untouched, and the next valid call on the same handle gives the right factors."""
+    import ctypes
+    import torch
+    from paper_1611_06365_b200 import _capi
+    pool = mla.default_pool()
+    n = 1200
+    a = gen(n, n, 31)
+    pristine = torch.from_numpy(np.array(a.T, order="C", copy=True))
+    ipiv = torch.empty(n, dtype=torch.int32)
+    info = _capi.LuInfo()
+    call = _capi.lib().mla_getrf_la_host
+    try:
+        _set_host_phases(pool, [256, 512], 0)
+        for (m_, n_, ld_, b_o, b_i, variant, t_pf) in [(n - 1, n, n, 128, 32, 3, pool.t_pf),      # m < n
+                                                       (n, n, n - 8, 128, 32, 3, pool.t_pf),      # ld < m
+                                                       (n, n, n, 16, 32, 3, pool.t_pf),           # b_outer < b_inner
+                                                       (n, n, n, 2048, 32, 3, pool.t_pf),         # b_outer beyond a plan
+                                                       (n, n, n, 128, 32, 9, pool.t_pf),          # unknown variant
+                                                       (n, n, n, 128, 32, 3, pool.t)]:            # t_pf == t (lu.py:210-214)
+            host = pristine.clone().pin_memory()
+            rc = call(pool.handle, host.data_ptr(), m_, n_, ld_, ipiv.data_ptr(), b_o, b_i, variant, t_pf, 1, ctypes.byref(info))
+            assert rc == -1, (rc, m_, n_, ld_, b_o, b_i, variant, t_pf)
+            assert torch.equal(host, pristine)
+        host = pristine.clone().pin_memory()
+        rc = call(pool.handle, host.data_ptr(), n, n, n, ipiv.data_ptr(), 128, 32, _capi.VARIANT_CODES["lu_mb"], pool.t_pf, 1,
+                  ctypes.byref(info))
+        _capi.check(rc, pool.handle, "mla_getrf_la_host")
+        d = mla.from_numpy(a)
+        r = mla.lu_la(d, mla.Policy("lu_mb", mla.BlockConfig(128, 32)), pool)
+        assert np.array_equal(ipiv.numpy().astype(np.int64), r.ipiv.ipiv)
+        assert np.array_equal(host.numpy().T, mla.to_numpy(d))
+    finally:
+        _set_host_phases(pool, None, 4096)
+
+
 def test_host_entry_default_windows_at_config2_size(mla):
     """The default window policy (n/32, n/8, 3n/8; deep catch-up) is active from n = 8192: config 2's matrix
     through the host entry point against the reference-pinned golden pivots and the device path's factors."""
