@@ -377,17 +377,23 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
               } else {
                 ld_b128(&slots[wrank].rv[cc], lo, hi);
               }
+              // the diagonal row was requested before the headers were polled and may have come back stale: ask
+              // again NOW, next to the winner's row, so that the two answers travel together instead of one
+              // round trip after the other
+              // (only the CTA that holds the pivot row needs the diagonal row's values at all)
+              const bool need_dg = (p != jc) && (p >= r0 && p < r1);
+              unsigned long long lo2 = dlo, hi2 = dhi;
+              if (need_dg && (cc >= 32 || (unsigned)hi2 != seq)) ld_b128(&slots[drank].dg[cc], lo2, hi2);
               if ((unsigned)hi != seq && !poll_unit(&slots[wrank].rv[cc], seq, team.abort_word, lo, hi)) { good = false; break; }
               double uu = __longlong_as_double((long long)lo);
               ucur[cc] = uu;
               if (p != jc) {
-                unsigned long long lo2 = dlo, hi2 = dhi;
-                if (cc >= 32) ld_b128(&slots[drank].dg[cc], lo2, hi2);
-                if ((unsigned)hi2 != seq && !poll_unit(&slots[drank].dg[cc], seq, team.abort_word, lo2, hi2)) { good = false; break; }
-                double dd = __longlong_as_double((long long)lo2);
                 // interchange rows jc <-> p inside the block (lu.py:60-64)
                 if (own_diag) Sb[(int64_t)cc * lds + (jc - r0)] = uu;
-                if (p >= r0 && p < r1) Sb[(int64_t)cc * lds + (p - r0)] = dd;
+                if (need_dg) {
+                  if ((unsigned)hi2 != seq && !poll_unit(&slots[drank].dg[cc], seq, team.abort_word, lo2, hi2)) { good = false; break; }
+                  Sb[(int64_t)cc * lds + (p - r0)] = __longlong_as_double((long long)lo2);
+                }
               }
             }
             good = __all_sync(0xffffffffu, good);
