@@ -42,9 +42,12 @@ struct GemmCfg {
 };
 
 using GemmUpdateCfg = GemmCfg<128, 128, 2, 4, 3, 32>;  // trailing update tiles
-using GemmPanelCfg = GemmCfg<128, 32, 8, 1, 4>;    // panel-internal update (N = inner block)
-using GemmPanel16Cfg = GemmCfg<128, 16, 8, 1, 4>;  // same, for blocks narrowed to 16 columns (slab fitting)
-using GemmPanel8Cfg = GemmCfg<128, 8, 8, 1, 4>;    // ... and to 8 columns (very tall panels)
+// Panel-internal update (N = the panel's device block: 32 columns, or 16 / 8 after slab fitting).  32-deep slices in a
+// 2-stage ring: the same shared memory as four 16-deep stages, half as many barriers per tile -- these narrow
+// tiles are bound by the latency around each slice, not by the DMMA pipe (panel gemm -5 %, round 2).
+using GemmPanelCfg = GemmCfg<128, 32, 8, 1, 2, 32>;
+using GemmPanel16Cfg = GemmCfg<128, 16, 8, 1, 2, 32>;
+using GemmPanel8Cfg = GemmCfg<128, 8, 8, 1, 2, 32>;
 using GemmTrsmCfg = GemmCfg<32, 128, 1, 8, 4>;     // row-block update inside trsm strips
 
 // Issue the cp.async loads of k-tile `kt` into ring slot `slot`.

@@ -506,25 +506,28 @@ __device__ inline PanelResult panel_ll(Team& team, double* P, int m, int w, int6
     MLA_PROF(2);
     if (rank == 0 && tid == 0) ws->prof[5] += xchg_acc;
     // ---- write the slab back, record pivots ------------------------------------------------------
-    if (resident) {
-      for (int x = tid; x < nrows * wb; x += kThreads) {
-        int c = x / nrows, i = x - c * nrows;
-        P[(int64_t)(j + c) * ld + r0 + i] = Sb[(int64_t)c * lds + i];
-      }
-    }
     if (tid < wb) {
       sh.piv_rel[tid] = sh.piv[tid] - j;
       if (rank == 0) ipiv_out[j + tid] = sh.piv[tid];
     }
     __syncthreads();
+    // warp 0 resolves the block's interchanges into a plan (a serial chain over the wb pivots) WHILE warps 1-7
+    // write the slab back; both are needed before step 4
+    const bool want_plan = (w - wb > 0);
+    if (warp == 0 && want_plan) {
+      PlanRef pr{&sh.plan_count, sh.plan_dst, sh.plan_src};
+      build_pivot_plan(sh.piv_rel, wb, (int64_t)(m - j), false, pr, sh.plan_top, sh.plan_keys, sh.plan_vals,
+                       2 * kMaxInner, sh.plan_pv);
+    } else if (resident) {
+      const int t0 = want_plan ? tid - 32 : tid, nt = want_plan ? kThreads - 32 : kThreads;
+      for (int x = t0; x < nrows * wb; x += nt) {
+        int c = x / nrows, i = x - c * nrows;
+        P[(int64_t)(j + c) * ld + r0 + i] = Sb[(int64_t)c * lds + i];
+      }
+    }
+    __syncthreads();
     // ---- 4. the block's interchanges reach the other panel columns ------------------------------
     if (w - wb > 0) {
-      if (warp == 0) {
-        PlanRef pr{&sh.plan_count, sh.plan_dst, sh.plan_src};
-        build_pivot_plan(sh.piv_rel, wb, (int64_t)(m - j), false, pr, sh.plan_top, sh.plan_keys, sh.plan_vals,
-                         2 * kMaxInner, sh.plan_pv);
-      }
-      __syncthreads();
       PlanRef pr{&sh.plan_count, sh.plan_dst, sh.plan_src};
       const int oc = w - wb;  // other columns: [0,j) then [j+wb, w)
       int share = (oc + T - 1) / T;
