@@ -36,10 +36,10 @@ from paper_1611_06365_b200.workloads import CONFIGS, flops_lu, make_matrix  # no
 
 # DRAM bytes of ONE k_getrf launch on the default workload (n=32768, b=512/64, lu_et, sm_pf 32), from
 # `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` (profiles/r02_getrf_n32768_traffic.csv):
-# 496.2 GB read + 232.0 GB written; the algorithmic minimum (the trailing matrix read and written once
+# 491.8 GB read + 231.0 GB written; the algorithmic minimum (the trailing matrix read and written once
 # per iteration) is 2 * 8 * n^3 / (3 b) = 367 GB at b = 512 (ET cuts make the effective b smaller).
 # It cannot be measured by the run that prints it (ncu replays the launch), hence the constant + its source.
-DEFAULT_WORKLOAD_DRAM_BYTES = 496217638144 + 232044861440
+DEFAULT_WORKLOAD_DRAM_BYTES = 491778257664 + 231039581696
 DEFAULT_WORKLOAD_DRAM_SOURCE = ("profiles/r02_getrf_n32768_traffic.csv (ncu dram__bytes_read.sum + dram__bytes_write.sum of "
                                 "the k_getrf launch of this same command, captured in a separate run under ncu)")
 
