@@ -364,12 +364,18 @@ def _check_against_fixture(mla, name, a, ipiv, what):
     g = np.load(os.path.join(GOLDEN_DIR, f"golden_{name}.npz"))
     d0 = first_pivot_difference(ipiv, g["ipiv"])
     assert d0 is None, f"{what}: first differing pivot {d0}"
+    # Tolerance of check (b): 1e-10 against a fixture made by the pinned oracle (the reference's own arithmetic).
+    # The n = 65536 fixture comes from LAPACK getrf instead -- a second oracle with its own blocking and
+    # summation order, which itself sits 6e-11 away from the pinned oracle at n = 32768 (diag(U),
+    # make_golden_lapack.py --check); every variant lands at 0.99e-10 ... 1.03e-10 of it
+    # (lu_et: depending on the ET width schedule).  Against that fixture the bound is therefore 2e-10.
+    tol = 2.0 * LU_RTOL if str(g["pinned_by"][0]).startswith("lapack") else LU_RTOL
     if "sample_idx" in g.files:
         idx = torch.from_numpy(g["sample_idx"]).to(a.device)
         err = sampled_lu_error(a[idx, :].cpu().numpy(), a[:, idx].cpu().numpy(), g)
-        assert err <= LU_RTOL, f"{what}: sampled rows/columns differ by {err:.3e} (column-scaled)"
+        assert err <= tol, f"{what}: sampled rows/columns differ by {err:.3e} (column-scaled), bound {tol:.1e}"
     diag = torch.diagonal(a).cpu().numpy()
-    assert np.abs(diag - g["diag"]).max() <= LU_RTOL * np.abs(g["diag"]).max()
+    assert np.abs(diag - g["diag"]).max() <= tol * np.abs(g["diag"]).max()
 
 
 def _full_config(mla, name, variant="lu_et", b=None, oracle_full=False):
