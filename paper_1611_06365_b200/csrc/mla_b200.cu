@@ -507,7 +507,7 @@ int mla_launch_getrf_traced(const GetrfArgs& a, int grid, int smem_bytes, cudaSt
 // host entry point -- columns [0, k0) are factored and applied, LuState carries on, a raised abort word stays).
 static int getrf_launch(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
                         int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
-                        int32_t* widths, int widths_cap, int64_t k0, void* stream);
+                        int32_t* widths, int widths_cap, int64_t k0, void* stream, int first_by_all = 0);
 
 extern "C" int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
                             int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
@@ -517,7 +517,7 @@ extern "C" int mla_getrf_la(mla_handle h, double* A, int64_t m, int64_t n, int64
 
 static int getrf_launch(mla_handle h, double* A, int64_t m, int64_t n, int64_t ld, int32_t* ipiv, int b_outer,
                         int b_inner, int variant, int sm_pf, int q_chunks, mla_lu_info* info_dev,
-                        int32_t* widths, int widths_cap, int64_t k0, void* stream) {
+                        int32_t* widths, int widths_cap, int64_t k0, void* stream, int first_by_all) {
   if (!h || m < n || n < 0 || (m > 0 && ld < m) || k0 < 0 || (k0 > 0 && k0 >= n)) return MLA_E_INVALID;
   if (b_inner < 1 || b_outer < b_inner || b_outer > kMaxPiv) return MLA_E_INVALID;
   if (variant < MLA_VARIANT_LU || variant > MLA_VARIANT_LU_ET) return MLA_E_INVALID;
@@ -538,7 +538,7 @@ static int getrf_launch(mla_handle h, double* A, int64_t m, int64_t n, int64_t l
   }
   GetrfArgs a{A, (int)m, (int)n, ld, ipiv, b_outer, b_inner, variant, sm_pf, q_chunks < 1 ? 1 : q_chunks,
               h->sm_pf_max, h->next_progress, h->lu_state, h->plan, h->panel_ws, h->piv_local, h->ctrl, info_dev, widths, widths_cap,
-              h->trace_dev, h->dinv, (int)k0};
+              h->trace_dev, h->dinv, (int)k0, first_by_all};
   h->next_progress = nullptr;
   int e = h->trace_dev ? mla_launch_getrf_traced(a, grid, kDynSmemBytes, s) : mla_launch_getrf(a, grid, kDynSmemBytes, s);
   if (e != 0) { h->last_cuda = e; return MLA_E_CUDA; }
@@ -729,7 +729,7 @@ static int getrf_la_host_impl(mla_handle h, double* A_host, int64_t m, int64_t n
     if (timeline) cudaEventRecord(tl[3 * g + 1], s);
     h->next_progress = (g == np - 1) ? h->progress_dev : nullptr;
     rc = getrf_launch(h, h->a_dev, m, c1, ld, h->ipiv_dev, b_outer, b_inner, variant, sm_pf, q_chunks, h->info_dev,
-                      nullptr, 0, c0, s);
+                      nullptr, 0, c0, s, h->phase_deep > 0 ? 1 : 0);
     h->next_progress = nullptr;
     if (rc != MLA_OK) return rc;
     if (timeline) cudaEventRecord(tl[3 * g + 2], s);

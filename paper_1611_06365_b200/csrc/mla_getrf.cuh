@@ -104,6 +104,10 @@ struct GetrfArgs {
   // columns left of k0 (LEFT items), and the outcome counters / iteration numbering in LuState carry on from
   // the previous launch (the host does not reset LuState).  k0 == 0: a fresh factorization.
   int k0;
+  // A later window's first panel: by the panel team (0; the factors then do not depend on where the windows are
+  // cut) or by the whole grid like the very first panel (1; faster -- nothing else can run beside it anyway --
+  // and used when the caller has given up bit-identity with the unwindowed run, i.e. with deep catch-up).
+  int window_first_by_all;
 };
 
 // item counts of one iteration, derived identically by every CTA from the descriptor
@@ -565,7 +569,7 @@ __device__ __forceinline__ void getrf_persistent(const GetrfArgs& a, double* sme
     const int w0 = imin(a.b_outer, n - k0);
     double* const P0 = a.A + (int64_t)k0 * a.ld + k0;
     const int it_first = ks.it_next;
-    if (k0 > 0 && la) {
+    if (k0 > 0 && la && !a.window_first_by_all) {
       if (bid < ks.sm_pf) {
         tr_begin();
         Team t = team_pf();
